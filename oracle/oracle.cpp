@@ -79,9 +79,14 @@ double log_bessel_k_integral(double nu, double z) {
   double curv = z * std::cosh(tstar);
   double sigma = 1.0 / std::sqrt(curv + 1.0);
   double h = std::min(0.02, sigma / 24.0);
-  // locate the maximum on a grid first (robust, f is unimodal in t >= 0)
-  double fmax = f(0.0);
-  for (double t = 0.0; t < tstar + 20.0 * sigma + 1.0; t += h) fmax = std::max(fmax, f(t));
+  // locate the maximum by ternary search (f is unimodal on t >= 0: f'(0) = 0 and
+  // f' = −z sinh t + nu tanh(nu t) changes sign at most once)
+  double lo = 0.0, hi = tstar + 20.0 * sigma + 1.0;
+  for (int it = 0; it < 200; ++it) {
+    const double m1 = lo + (hi - lo) / 3.0, m2 = hi - (hi - lo) / 3.0;
+    if (f(m1) < f(m2)) lo = m1; else hi = m2;
+  }
+  const double fmax = std::max(f(0.0), f(0.5 * (lo + hi)));
   // trapezoid over [0, T]; the integrand is even so the t = 0 node has weight 1/2
   double sum = 0.5 * std::exp(f(0.0) - fmax);
   double t = h;
