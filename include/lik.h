@@ -1,0 +1,135 @@
+/* ==========================================================================
+ * lik.h — C ABI of the B200 (sm_100a) batched profile-likelihood library
+ * (liblik.so, built from paper_2305_04318_b200/csrc/).
+ *
+ * What it computes (arXiv 2305.04318, PAPER.md "P:<line>"):
+ *   For every correlation-parameter point ω_k = (φX, κ, ν², φR, φA) and every
+ *   Box-Cox λ_m, the Gaussian linear geostatistical model profile
+ *   log-likelihood ℓ_p(ω_k, λ_m; y) of Eq. (profile), P:145-148:
+ *
+ *     −2ℓ_p = n log(q/n) + log|V| − 2(λ−1) Σ log y_i + n log(2π) + n,
+ *     q     = (y' − Xβ̂)ᵀ V⁻¹ (y' − Xβ̂)              (Eq. 4,  P:141)
+ *     β̂     = (XᵀV⁻¹X)⁻¹ XᵀV⁻¹ y'                     (Eq. betahat)
+ *     σ̂²    = q / n                                   (Eq. 4,  P:141)
+ *     y'    = b(y; λ) = (y^λ − 1)/λ, log y at λ = 0   (§2)
+ *     V     = R + ν² I, R_ij = ρ(s_i − s_j)           (Eq. 1 block)
+ *     ρ(x)  = 2^{1−κ}/Γ(κ) (√(8κ) d)^κ K_κ(√(8κ) d)   (Eq. matern, P:100-103;
+ *             prefactor read as 2^{1−κ}, R1)
+ *     d(x)  = ‖diag(1/φX, 1/φY) Rot(φA) x‖, φY = φX/φR (R3)
+ *
+ *   following the paper's Steps 1-8 (§3.3): Matérn matrix, Cholesky
+ *   of V with log|V|, triangular solve against [y'_1..y'_M | X], the cross
+ *   products (Table 1), the p×p Cholesky of XᵀV⁻¹X, β̂, ssqBetahat
+ *   and ssqResidual.  All M λ share one factorisation per point.
+ *
+ * Conventions (all entry points):
+ *   - FP64 everywhere; matrices row-major; all buffers caller-owned (the
+ *     library never frees or retains caller memory beyond the call).
+ *   - coords: n×2 (x_i, y_i); y: n, all > 0; X: n×p (full column rank);
+ *     params: K×5 {φX, κ, ν², φR, φA [radians]}; lambdas: M.
+ *   - outputs: loglik K×M (ℓ_p, not −2ℓ_p), betahat K×M×p, sigma2hat K×M,
+ *     logdetV K, status K (LIK_PT_*).
+ *   - limits: 1 ≤ p, n ≥ p + 2, K ≥ 1, M ≥ 1, M + p ≤ 64.
+ *   - Call-level errors return < 0, write no outputs, and set the message
+ *     returned by lik_last_error (naming the offending index).
+ *   - Point-level failures never fail the call: status[k] != 0,
+ *     loglik[k,·] = −inf, betahat/sigma2hat = NaN, logdetV[k] = NaN
+ *     (for LIK_PT_NEG_RESID only the failing λ columns are −inf / NaN).
+ *   - Results are bitwise deterministic for given inputs, independent of K,
+ *     the wave size, the stream and the number of GPUs.
+ *   - One lik_ctx per host thread; a ctx is bound to one CUDA device.
+ * ========================================================================== */
+#ifndef LIK_H_
+#define LIK_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lik_ctx lik_ctx; /* opaque */
+
+/* Call-level return codes. */
+enum {
+  LIK_OK = 0,
+  LIK_EINVAL = -1,   /* NULL pointer, bad sizes (n < p+2, p < 1, K < 1, M < 1, M+p > 64),
+                        non-finite coords / y / X / lambdas */
+  LIK_EDOMAIN = -2,  /* some y_i <= 0 (Box-Cox needs log y) or two coincident sites */
+  LIK_ERANK = -3,    /* X not of full column rank */
+  LIK_ENOMEM = -4,   /* device workspace allocation failed */
+  LIK_ECUDA = -5,    /* a CUDA runtime error (message has the CUDA error string) */
+  LIK_ENOTIMPL = -6  /* entry point or option not implemented */
+};
+
+/* Per-point status codes (status[k]). */
+enum {
+  LIK_PT_OK = 0,
+  LIK_PT_V_NOT_PD = 1,    /* a Cholesky pivot of V <= n·eps·max V_ii (R11) */
+  LIK_PT_XVX_NOT_PD = 2,  /* a pivot of XᵀV⁻¹X <= p·eps·max diag (Step 5) */
+  LIK_PT_NEG_RESID = 3,   /* ssqResidual = ssqYX − ssqBetahat < −1e-8·ssqYX (Step 8, R12) */
+  LIK_PT_BAD_PARAM = 4    /* φX <= 0, κ <= 0, ν² < 0, φR <= 0 or a non-finite parameter */
+};
+
+/* lik_create flags */
+#define LIK_FLAG_TIMING 1u /* record CUDA events around every kernel launch (lik_get_stage_times) */
+
+/* Stages reported by lik_get_stage_times. */
+enum {
+  LIK_STAGE_PREP = 0,   /* Box-Cox columns, Σ log y (a1) */
+  LIK_STAGE_SETUP = 1,  /* per-point constants (a2 prologue) */
+  LIK_STAGE_BUILD = 2,  /* matern_build: V tiles + [y'|X]ᵀ rows (a2) */
+  LIK_STAGE_CHOL = 3,   /* chol_fused: Cholesky, solve, cross products, epilogue (a3-a7) */
+  LIK_NSTAGES = 4
+};
+
+/* Create a context on CUDA device `cuda_device` (ordinal in the process's
+ * visible set).  *out receives the context.  Returns LIK_OK, LIK_EINVAL
+ * (out == NULL, unknown flag) or LIK_ECUDA (no such device / not sm_100). */
+int lik_create(lik_ctx** out, int cuda_device, unsigned flags);
+
+/* Release the context and its device workspace.  NULL is a no-op. */
+void lik_destroy(lik_ctx* ctx);
+
+/* Message describing the last non-OK return on this context ("" if none).
+ * The pointer stays valid until the next call on ctx. */
+const char* lik_last_error(const lik_ctx* ctx);
+
+/* Batched evaluation, HOST pointers (the north_star's lik_eval_batch).
+ * Copies the inputs to the device, runs the whole path on the context's own
+ * stream, copies the outputs back and synchronises before returning. */
+int lik_eval_batch(lik_ctx* ctx, int n, int p, const double* coords, const double* y,
+                   const double* X, int K, const double* params, int M, const double* lambdas,
+                   double* loglik, double* betahat, double* sigma2hat, double* logdetV,
+                   int* status);
+
+/* Same arguments, all DEVICE pointers (on ctx's device), enqueued on
+ * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream).  The
+ * dataset (coords, y, X: ≤ n·(3+p) doubles) is read back to the host for the
+ * call-level validation, so the call synchronises once on entry; the hot path
+ * is then enqueued and the call returns without waiting for it (unless
+ * LIK_FLAG_TIMING is set, in which case it waits to read the events). */
+int lik_eval_batch_device(lik_ctx* ctx, int n, int p, const double* coords, const double* y,
+                          const double* X, int K, const double* params, int M,
+                          const double* lambdas, double* loglik, double* betahat,
+                          double* sigma2hat, double* logdetV, int* status, void* cuda_stream);
+
+/* Accumulated per-stage device time (ms, from CUDA events on the launching
+ * stream) and launch counts since the last reset; arrays of LIK_NSTAGES.
+ * Requires LIK_FLAG_TIMING (else LIK_EINVAL). */
+int lik_get_stage_times(lik_ctx* ctx, double* ms, long long* launches);
+int lik_reset_stage_times(lik_ctx* ctx);
+
+/* Points processed concurrently per wave (0 = automatic: one per SM slot,
+ * bounded by free HBM).  Results do not depend on it (determinism tests). */
+int lik_set_wave_points(lik_ctx* ctx, int points_per_wave);
+
+/* Debug / parity entry: the dense V = R + ν²I (n×n full, row-major) for each
+ * of K points, written by the same matern_build kernel the hot path uses.
+ * Device pointers; synchronous.  Same validation as lik_eval_batch_device
+ * for n, coords and params (bad points give an all-NaN matrix). */
+int lik_debug_build_V(lik_ctx* ctx, int n, const double* coords, int K, const double* params,
+                      double* V);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIK_H_ */

@@ -1,0 +1,464 @@
+// chol_fused — one CTA per parameter point: the paper's Steps 2-8 (§3.3,
+// P:312-323) on the augmented matrix  A = [[V, B], [Bᵀ, 0]],  B = [y'|X].
+//
+// Left-looking (Crout) blocked Cholesky over 64×64 tiles:
+//   for tile column j:   for row blocks (two tile rows at a time, i ≥ j, then the
+//   augmented row):
+//     C  = A_ij − Σ_{k<j} L_ik L_jkᵀ            (FP64 DMMA.8x8x4 tensor cores)
+//     i = j:  C = L_jj L_jjᵀ (unblocked, shared memory), log|V| += Σ log pivots,
+//             L_jj⁻¹ for the solves of this column
+//     i > j:  L_ij = C L_jj⁻ᵀ                   (DMMA)
+// The augmented row ends up holding Zᵀ = (L⁻¹B)ᵀ (Step 3), and its final
+// diagonal block  −Σ_k Z_k Z_kᵀ = −BᵀV⁻¹B  is the cross-product matrix ssqYX of
+// Table 1 (Step 4).  The epilogue does Steps 5-8 and Eq. (profile).
+//
+// Operand staging: tiles are stored as contiguous 64×32 swizzled chunks
+// (lik_internal.cuh), so each pipeline stage is three 1-D bulk copies
+// (cp.async.bulk, the TMA engine) completing on an mbarrier; a 3-stage ring.
+// 256 threads = 8 warps as 4 (32-row) × 2 (32-column) warp tiles of a 128×64
+// row block; each warp owns 4×4 DMMA 8×8 accumulators.
+#include <cfloat>
+#include <cstdint>
+#include "../../include/lik.h"
+#include "lik_internal.cuh"
+
+namespace lik {
+namespace {
+
+constexpr int NT = 256;
+constexpr int NSTAGE = 3;
+constexpr int STAGE_D = 3 * CHUNK_D;  // A rows of tile a, A rows of tile b, B rows
+constexpr int OFF_LINV = NSTAGE * STAGE_D;
+constexpr int OFF_DLOG = OFF_LINV + TILE_D;
+constexpr int OFF_MISC = OFF_DLOG + 64;          // 8 doubles of scalars
+constexpr int OFF_MBAR = OFF_MISC + 8;           // NSTAGE uint64
+constexpr int SMEM_D = OFF_MBAR + NSTAGE + 4;    // + int flags
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+}
+
+typedef double Acc[4][4][2];
+
+// One 64×32 chunk (8 k-steps of 4) of  acc += A_rows · B_rowsᵀ  for this warp.
+__device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ Ab, int rbase,
+                                          int mlim, const double* __restrict__ Bb, int cbase,
+                                          int lane) {
+  const int lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int kcol = ((kk * 4) ^ sw) + lc;
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bb[(cbase + ni * 8 + lr) * KC + kcol];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+      if (mi < mlim) {
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+  }
+}
+
+__device__ __forceinline__ void frag_load(Acc& acc, const double* __restrict__ T, int rbase,
+                                          int cbase, int mlim, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      if (mi < mlim) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc));
+        acc[mi][ni][0] = v.x;
+        acc[mi][ni][1] = v.y;
+      } else {
+        acc[mi][ni][0] = 0.0;
+        acc[mi][ni][1] = 0.0;
+      }
+    }
+}
+
+__device__ __forceinline__ void frag_store(const Acc& acc, double* __restrict__ T, int rbase,
+                                           int cbase, int mlim, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+    if (mi < mlim) {
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        double2 v;
+        v.x = acc[mi][ni][0];
+        v.y = acc[mi][ni][1];
+        *reinterpret_cast<double2*>(T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc)) = v;
+      }
+    }
+}
+
+__device__ __forceinline__ void frag_zero(Acc& acc) {
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+}
+
+struct Pipe {
+  double* stages;
+  uint64_t* mbar;
+  uint32_t seq;  // chunks consumed so far (same value in every thread)
+};
+
+// acc -= (or +=) Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
+//   A rows of tile a: gA0 + q·CHUNK_D (cA0 rows copied), tile b: gA1 (cA1 rows),
+//   B rows: gB (cB rows).  The accumulation sign is folded in by the caller
+//   (acc starts at −A_ij and the result is negated) — here acc += A Bᵀ.
+__device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int cA0,
+                                      const double* gA1, int cA1, const double* gB, int cB,
+                                      int nq, bool mine_b, int rbase, int mlim, int cbase,
+                                      int lane) {
+  const int tid = threadIdx.x;
+  const uint32_t seq = pp.seq;
+  auto issue = [&](int q) {
+    const uint32_t s = (seq + q) % NSTAGE;
+    double* st = pp.stages + s * STAGE_D;
+    const uint32_t bar = saddr(&pp.mbar[s]);
+    mbar_expect_tx(bar, (uint32_t)(cA0 + cA1 + cB) * KC * 8);
+    bulk_g2s(saddr(st), gA0 + (size_t)q * CHUNK_D, cA0 * KC * 8, bar);
+    if (cA1) bulk_g2s(saddr(st + CHUNK_D), gA1 + (size_t)q * CHUNK_D, cA1 * KC * 8, bar);
+    bulk_g2s(saddr(st + 2 * CHUNK_D), gB + (size_t)q * CHUNK_D, cB * KC * 8, bar);
+  };
+  if (tid == 0) {
+    issue(0);
+    if (nq > 1) issue(1);
+  }
+  for (int q = 0; q < nq; ++q) {
+    if (tid == 0 && q + 2 < nq) issue(q + 2);
+    const uint32_t s = (seq + q) % NSTAGE;
+    mbar_wait(saddr(&pp.mbar[s]), ((seq + q) / NSTAGE) & 1);
+    const double* st = pp.stages + s * STAGE_D;
+    if (mlim > 0) mma_chunk(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, cbase, lane);
+    __syncthreads();
+  }
+  pp.seq = seq + nq;
+}
+
+// Unblocked Cholesky of the leading v×v block of a 64×64 tile in shared memory
+// (lower part used; rows/columns ≥ v are the identity padding and are never
+// read).  dlog[c] = log(pivot_c) = 2 log L_cc.  Returns nonzero (uniformly) if
+// a pivot is ≤ tol (R11).
+__device__ int potrf64(double* S, int v, double tol, double* dlog, double* scal, int* flag) {
+  const int tid = threadIdx.x;
+  for (int c = 0; c < v; ++c) {
+    if (tid == 0) {
+      const double d = S[sw_off(c, c)];
+      if (!(d > tol)) {
+        flag[0] = 1;
+      } else {
+        const double l = sqrt(d);
+        dlog[c] = log(d);
+        S[sw_off(c, c)] = l;
+        scal[0] = 1.0 / l;
+      }
+    }
+    __syncthreads();
+    if (flag[0]) return 1;
+    const double inv = scal[0];
+    for (int r = c + 1 + tid; r < v; r += NT) S[sw_off(r, c)] *= inv;
+    __syncthreads();
+    for (int e = tid; e < TILE_D; e += NT) {
+      const int rr = e >> 6, kk = e & 63;
+      if (kk > c && kk <= rr && rr < v) S[sw_off(rr, kk)] -= S[sw_off(rr, c)] * S[sw_off(kk, c)];
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// X = L⁻¹ for the leading v×v block (column-wise forward substitution); the
+// padded block of X is the identity, so the solves leave padded columns of the
+// right-hand side (which are zero) unchanged.
+__device__ void trinv64(const double* S, int v, double* X) {
+  const int c = threadIdx.x;
+  if (c < TB) {
+    for (int i = 0; i < TB; ++i) {
+      double x;
+      if (i < c) {
+        x = 0.0;
+      } else if (c >= v || i >= v) {
+        x = (i == c) ? 1.0 : 0.0;
+      } else {
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int k = c; k < i; ++k) s -= S[sw_off(i, k)] * X[sw_off(k, c)];
+        x = s / S[sw_off(i, i)];
+      }
+      X[sw_off(i, c)] = x;
+    }
+  }
+}
+
+__device__ void write_point_failure(const CholArgs& A, int k, int code) {
+  const int tid = threadIdx.x;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  for (int e = tid; e < A.M; e += NT) {
+    A.loglik[(size_t)k * A.M + e] = -INFINITY;
+    A.sigma2hat[(size_t)k * A.M + e] = nan;
+  }
+  for (int e = tid; e < A.M * A.p; e += NT) A.betahat[(size_t)k * A.M * A.p + e] = nan;
+  if (tid == 0) {
+    A.logdetV[k] = nan;
+    A.status[k] = code;
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
+  extern __shared__ __align__(1024) double sm[];
+  double* staging = sm;  // aliases the stage ring (used only between k-loops)
+  double* Linv = sm + OFF_LINV;
+  double* dlog = sm + OFF_DLOG;
+  double* scal = sm + OFF_MISC;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + OFF_MBAR);
+  int* flag = reinterpret_cast<int*>(sm + OFF_MBAR + NSTAGE);
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = w >> 1, wc = w & 1;
+  const int rbase = (wr & 1) * 32, cbase = wc * 32;
+  const bool mine_b = wr >= 2;
+  const int k = A.k0 + blockIdx.x;
+  const SlotGeom g = A.g;
+  const int nt = g.nt, M = A.M, p = A.p, r = g.r;
+  double* ws = A.ws + (size_t)blockIdx.x * g.slot_d;
+  const PointConst P = A.pc[k];
+
+  if (P.mode == MODE_BAD) {
+    write_point_failure(A, k, LIK_PT_BAD_PARAM);
+    return;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(saddr(&mbar[s]), 1);
+    flag[0] = flag[1] = flag[2] = 0;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  Pipe pp{sm, mbar, 0u};
+  const double tol = g.n * DBL_EPSILON * (1.0 + P.nugget);
+  double logdet = 0.0;  // meaningful in thread 0
+  auto valid_rows = [&](int ti) { return ti == nt ? g.Ra : (ti == nt - 1 ? g.vlast : TB); };
+  auto copy_rows = [&](int ti) { return ti == nt ? g.Ra : TB; };
+  auto tile_ptr = [&](int ti, int tj) -> double* {
+    return ws + (size_t)(ti == nt ? g.ntri + tj : tri_index(ti, tj)) * TILE_D;
+  };
+
+  Acc acc;
+  for (int j = 0; j < nt; ++j) {
+    const int nrow = nt - j + 1;  // tile rows j..nt-1 and the augmented row
+    for (int rb = 0; rb < nrow; rb += 2) {
+      const int ia = j + rb;
+      const int ib = (rb + 1 < nrow) ? j + rb + 1 : -1;
+      const int vmine = mine_b ? (ib >= 0 ? valid_rows(ib) : 0) : valid_rows(ia);
+      const int mlim = max(0, min(4, (vmine - rbase + 7) >> 3));
+      // C = A_ij − Σ_k L_ik L_jkᵀ, accumulated as acc = −A_ij + Σ L Lᵀ, negated below
+      if (mlim > 0) {
+        frag_load(acc, tile_ptr(mine_b ? ib : ia, j), rbase, cbase, mlim, lane);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            acc[mi][ni][0] = -acc[mi][ni][0];
+            acc[mi][ni][1] = -acc[mi][ni][1];
+          }
+      } else {
+        frag_zero(acc);
+      }
+      if (j > 0)
+        kloop(acc, pp, tile_ptr(ia, 0), copy_rows(ia), ib >= 0 ? tile_ptr(ib, 0) : nullptr,
+              ib >= 0 ? copy_rows(ib) : 0, tile_ptr(j, 0), TB, 2 * j, mine_b, rbase, mlim, cbase,
+              lane);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          acc[mi][ni][0] = -acc[mi][ni][0];
+          acc[mi][ni][1] = -acc[mi][ni][1];
+        }
+      __syncthreads();
+      frag_store(acc, staging + (mine_b ? TILE_D : 0), rbase, cbase, mlim, lane);
+      __syncthreads();
+      if (rb == 0) {
+        // diagonal tile: factor, log-determinant, inverse for this column's solves
+        if (potrf64(staging, valid_rows(j), tol, dlog, scal, flag)) {
+          write_point_failure(A, k, LIK_PT_V_NOT_PD);
+          return;
+        }
+        if (tid == 0) {
+          double s = 0.0;
+          for (int c = 0; c < valid_rows(j); ++c) s += dlog[c];
+          logdet += s;
+        }
+        trinv64(staging, valid_rows(j), Linv);
+        __syncthreads();
+        if (ib >= 0 && mine_b) {
+          frag_zero(acc);
+          if (mlim > 0) {
+            mma_chunk(acc, staging + TILE_D, rbase, mlim, Linv, cbase, lane);
+            mma_chunk(acc, staging + TILE_D + CHUNK_D, rbase, mlim, Linv + CHUNK_D, cbase, lane);
+          }
+          frag_store(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
+        }
+      } else {
+        // L_ij = C L_jj⁻ᵀ for both tile rows of the block
+        frag_zero(acc);
+        const double* Sb = staging + (mine_b ? TILE_D : 0);
+        if (mlim > 0) {
+          mma_chunk(acc, Sb, rbase, mlim, Linv, cbase, lane);
+          mma_chunk(acc, Sb + CHUNK_D, rbase, mlim, Linv + CHUNK_D, cbase, lane);
+        }
+        const int ti = mine_b ? ib : ia;
+        if (ti >= 0) frag_store(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
+      }
+      fence_proxy_async();
+      __syncthreads();
+    }
+  }
+
+  // Final block of the augmented row: acc = Σ_k Z_k Z_kᵀ = BᵀV⁻¹B  (ssqYX, Table 1)
+  {
+    const int mlim = mine_b ? 0 : max(0, min(4, (g.Ra - rbase + 7) >> 3));
+    frag_zero(acc);
+    kloop(acc, pp, tile_ptr(nt, 0), g.Ra, nullptr, 0, tile_ptr(nt, 0), g.Ra, 2 * nt, false,
+          rbase, mlim, cbase, lane);
+    __syncthreads();
+    frag_store(acc, staging, rbase, cbase, mlim, lane);
+    __syncthreads();
+  }
+  // Steps 5-8 and Eq. (profile)
+  double* Cm = Linv;          // r×r, plain row-major with stride 64
+  double* Q = staging + TILE_D;  // p×p Cholesky factor of XᵀV⁻¹X (stride 64)
+  for (int e = tid; e < r * r; e += NT) {
+    const int a = e / r, b = e % r;
+    Cm[a * 64 + b] = staging[sw_off(a, b)];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double xmax = 0.0;
+    for (int a = 0; a < p; ++a) xmax = fmax(xmax, Cm[(M + a) * 64 + (M + a)]);
+    const double tolp = p * DBL_EPSILON * xmax;
+    int bad = 0;
+    for (int c = 0; c < p && !bad; ++c) {
+      double d = Cm[(M + c) * 64 + (M + c)];
+      for (int kk = 0; kk < c; ++kk) d -= Q[c * 64 + kk] * Q[c * 64 + kk];
+      if (!(d > tolp)) {
+        bad = 1;
+        break;
+      }
+      const double l = sqrt(d);
+      Q[c * 64 + c] = l;
+      for (int i = c + 1; i < p; ++i) {
+        double s = Cm[(M + i) * 64 + (M + c)];
+        for (int kk = 0; kk < c; ++kk) s -= Q[i * 64 + kk] * Q[c * 64 + kk];
+        Q[i * 64 + c] = s / l;
+      }
+    }
+    flag[1] = bad;
+    scal[1] = logdet;  // log|V| = Σ log pivots (Step 2)
+  }
+  __syncthreads();
+  if (flag[1]) {
+    write_point_failure(A, k, LIK_PT_XVX_NOT_PD);
+    return;
+  }
+  const double S = *A.S;
+  const double n = (double)g.n;
+  const double ldV = scal[1];
+  const double ln2pi = 1.8378770664093454836;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  for (int m = tid; m < M; m += NT) {
+    double cv[64], bt[64];
+    double sb = 0.0;
+    for (int a = 0; a < p; ++a) {  // Step 6: c = Q⁻¹ XᵀV⁻¹y'
+      double s = Cm[(M + a) * 64 + m];
+      for (int b = 0; b < a; ++b) s -= Q[a * 64 + b] * cv[b];
+      cv[a] = s / Q[a * 64 + a];
+      sb += cv[a] * cv[a];  // Step 7: ssqBetahat = cᵀc
+    }
+    const double yy = Cm[m * 64 + m];
+    double q = yy - sb;  // Step 8: ssqResidual
+    const bool neg = q < -1e-8 * yy;
+    if (!neg && q < 0.0) q = 0.0;  // R12
+    for (int a = p - 1; a >= 0; --a) {  // β̂ = Q⁻ᵀ c (Eq. betahat)
+      double s = cv[a];
+      for (int b = a + 1; b < p; ++b) s -= Q[b * 64 + a] * bt[b];
+      bt[a] = s / Q[a * 64 + a];
+    }
+    const size_t km = (size_t)k * M + m;
+    if (neg) {
+      A.loglik[km] = -INFINITY;
+      A.sigma2hat[km] = nan;
+      for (int a = 0; a < p; ++a) A.betahat[km * p + a] = nan;
+      atomicExch(&flag[2], 1);
+    } else {
+      const double s2 = q / n;  // Eq. 4
+      // Eq. (profile): −2ℓ_p = n log σ̂² + log|V| − 2(λ−1)Σ log y + n log 2π + n
+      A.loglik[km] = -0.5 * (n * log(s2) + ldV + n * ln2pi + n) + (A.lambdas[m] - 1.0) * S;
+      A.sigma2hat[km] = s2;
+      for (int a = 0; a < p; ++a) A.betahat[km * p + a] = bt[a];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    A.logdetV[k] = ldV;
+    A.status[k] = flag[2] ? LIK_PT_NEG_RESID : LIK_PT_OK;
+  }
+}
+
+}  // namespace
+
+size_t chol_smem_bytes() { return (size_t)SMEM_D * sizeof(double); }
+
+cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st) {
+  const size_t smem = chol_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(chol_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  chol_fused_kernel<<<kw, NT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace lik

@@ -1,0 +1,386 @@
+// C ABI of liblik.so (include/lik.h): validation, workspace, wave scheduling,
+// kernel launches and stage timing.  Host code only; every arithmetic step of
+// the likelihood runs in the CUDA kernels (matern_build.cu, chol_fused.cu).
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/lik.h"
+#include "lik_internal.cuh"
+
+using lik::PointConst;
+using lik::SlotGeom;
+
+struct lik_ctx {
+  int device = 0;
+  unsigned flags = 0;
+  int nsm = 0;
+  cudaStream_t own_stream = nullptr;
+  std::string err;
+  // device workspace (grown on demand)
+  double* ws = nullptr;
+  size_t ws_bytes = 0;
+  PointConst* pc = nullptr;
+  size_t pc_cap = 0;
+  double* bt = nullptr;
+  size_t bt_bytes = 0;
+  double* S = nullptr;
+  // host-API staging buffers
+  char* io = nullptr;
+  size_t io_bytes = 0;
+  int wave_points = 0;
+  // timing
+  double stage_ms[LIK_NSTAGES] = {0, 0, 0, 0};
+  long long stage_n[LIK_NSTAGES] = {0, 0, 0, 0};
+  std::vector<cudaEvent_t> ev;
+};
+
+namespace {
+
+int fail(lik_ctx* c, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+int fail(lik_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                                 \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? LIK_ENOMEM : LIK_ECUDA, "%s: %s", \
+                  #call, cudaGetErrorString(e_));                                           \
+  } while (0)
+
+template <class T>
+int ensure(lik_ctx* c, T** p, size_t* cap, size_t bytes) {
+  if (*cap >= bytes && *p) return LIK_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc((void**)p, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(c, LIK_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+  }
+  *cap = bytes;
+  return LIK_OK;
+}
+
+// Call-level validation on host copies of the (small) dataset.
+int validate(lik_ctx* c, int n, int p, const double* coords, const double* y, const double* X,
+             int K, int M, const double* lambdas) {
+  if (p < 1) return fail(c, LIK_EINVAL, "p = %d < 1", p);
+  if (n < p + 2) return fail(c, LIK_EINVAL, "n = %d < p + 2 = %d", n, p + 2);
+  if (K < 1) return fail(c, LIK_EINVAL, "K = %d < 1", K);
+  if (M < 1) return fail(c, LIK_EINVAL, "M = %d < 1", M);
+  if (M + p > 64) return fail(c, LIK_EINVAL, "M + p = %d > 64", M + p);
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(coords[2 * i]) || !std::isfinite(coords[2 * i + 1]))
+      return fail(c, LIK_EINVAL, "coords[%d] is not finite", i);
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(y[i])) return fail(c, LIK_EINVAL, "y[%d] is not finite", i);
+  for (long i = 0; i < (long)n * p; ++i)
+    if (!std::isfinite(X[i])) return fail(c, LIK_EINVAL, "X[%ld][%ld] is not finite", i / p, i % p);
+  for (int m = 0; m < M; ++m)
+    if (!std::isfinite(lambdas[m])) return fail(c, LIK_EINVAL, "lambdas[%d] is not finite", m);
+  for (int i = 0; i < n; ++i)
+    if (!(y[i] > 0.0)) return fail(c, LIK_EDOMAIN, "y[%d] = %g <= 0 (Box-Cox needs log y)", i, y[i]);
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) {
+    return coords[2 * a] < coords[2 * b] ||
+           (coords[2 * a] == coords[2 * b] && coords[2 * a + 1] < coords[2 * b + 1]);
+  });
+  for (int t = 1; t < n; ++t) {
+    const int a = idx[t - 1], b = idx[t];
+    if (coords[2 * a] == coords[2 * b] && coords[2 * a + 1] == coords[2 * b + 1])
+      return fail(c, LIK_EDOMAIN, "sites %d and %d coincide", std::min(a, b), std::max(a, b));
+  }
+  // full column rank of X (modified Gram-Schmidt, relative threshold)
+  std::vector<double> Q((size_t)n * p);
+  std::copy(X, X + (size_t)n * p, Q.begin());
+  for (int a = 0; a < p; ++a) {
+    double n0 = 0.0;
+    for (int i = 0; i < n; ++i) n0 += X[(size_t)i * p + a] * X[(size_t)i * p + a];
+    for (int b = 0; b < a; ++b) {
+      double d = 0.0;
+      for (int i = 0; i < n; ++i) d += Q[(size_t)i * p + a] * Q[(size_t)i * p + b];
+      for (int i = 0; i < n; ++i) Q[(size_t)i * p + a] -= d * Q[(size_t)i * p + b];
+    }
+    double nr = 0.0;
+    for (int i = 0; i < n; ++i) nr += Q[(size_t)i * p + a] * Q[(size_t)i * p + a];
+    if (n0 == 0.0 || !(nr > 1e-20 * n0))
+      return fail(c, LIK_ERANK, "X is not of full column rank (column %d)", a);
+    nr = std::sqrt(nr);
+    for (int i = 0; i < n; ++i) Q[(size_t)i * p + a] /= nr;
+  }
+  return LIK_OK;
+}
+
+cudaEvent_t ev_get(lik_ctx* c, size_t i) {
+  while (c->ev.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev.push_back(e);
+  }
+  return c->ev[i];
+}
+
+// The hot path on device buffers (inputs already validated).
+int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, const double* X,
+               int K, const double* params, int M, const double* lambdas, double* loglik,
+               double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st) {
+  const SlotGeom g = lik::make_geom(n, M + p);
+  const size_t slot_bytes = g.slot_d * sizeof(double);
+  int W = c->wave_points > 0 ? c->wave_points : c->nsm;
+  W = std::min(W, K);
+  {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t avail = fr + c->ws_bytes;
+    const size_t cap = (size_t)(0.85 * (double)avail) / slot_bytes;
+    if (cap < 1) return fail(c, LIK_ENOMEM, "one workspace slot (%zu bytes) exceeds free HBM", slot_bytes);
+    if ((size_t)W > cap) W = (int)cap;
+  }
+  int rc;
+  if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes))) return rc;
+  size_t pcb = c->pc_cap * sizeof(PointConst);
+  if ((rc = ensure(c, &c->pc, &pcb, (size_t)K * sizeof(PointConst)))) return rc;
+  c->pc_cap = pcb / sizeof(PointConst);
+  if ((rc = ensure(c, &c->bt, &c->bt_bytes, (size_t)g.r * g.nt * lik::TB * sizeof(double) + 64)))
+    return rc;
+  if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, sizeof(double)));
+
+  const bool timing = c->flags & LIK_FLAG_TIMING;
+  const int nwaves = (K + W - 1) / W;
+  size_t ei = 0;
+  if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+  CUDA_TRY(c, lik::launch_prep(y, X, lambdas, n, p, M, g.nt * lik::TB, c->bt, c->S, st));
+  if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+  CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
+  if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+  for (int w = 0; w < nwaves; ++w) {
+    const int k0 = w * W, kw = std::min(W, K - k0);
+    CUDA_TRY(c, lik::launch_build(coords, g, c->pc, k0, kw, c->bt, c->ws, st));
+    if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+    lik::CholArgs a;
+    a.ws = c->ws;
+    a.g = g;
+    a.M = M;
+    a.p = p;
+    a.pc = c->pc;
+    a.k0 = k0;
+    a.lambdas = lambdas;
+    a.S = c->S;
+    a.loglik = loglik;
+    a.betahat = betahat;
+    a.sigma2hat = sigma2hat;
+    a.logdetV = logdetV;
+    a.status = status;
+    CUDA_TRY(c, lik::launch_chol(a, kw, st));
+    if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+  }
+  if (timing) {
+    CUDA_TRY(c, cudaEventSynchronize(c->ev[ei - 1]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    c->stage_ms[LIK_STAGE_PREP] += ms;
+    c->stage_n[LIK_STAGE_PREP] += 1;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+    c->stage_ms[LIK_STAGE_SETUP] += ms;
+    c->stage_n[LIK_STAGE_SETUP] += 1;
+    for (int w = 0; w < nwaves; ++w) {
+      cudaEventElapsedTime(&ms, c->ev[2 + 2 * w], c->ev[3 + 2 * w]);
+      c->stage_ms[LIK_STAGE_BUILD] += ms;
+      cudaEventElapsedTime(&ms, c->ev[3 + 2 * w], c->ev[4 + 2 * w]);
+      c->stage_ms[LIK_STAGE_CHOL] += ms;
+    }
+    c->stage_n[LIK_STAGE_BUILD] += nwaves;
+    c->stage_n[LIK_STAGE_CHOL] += nwaves;
+  }
+  return LIK_OK;
+}
+
+bool any_null(std::initializer_list<const void*> ps) {
+  for (const void* q : ps)
+    if (!q) return true;
+  return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lik_create(lik_ctx** out, int cuda_device, unsigned flags) {
+  if (!out) return LIK_EINVAL;
+  *out = nullptr;
+  if (flags & ~LIK_FLAG_TIMING) return LIK_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
+    return LIK_ECUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return LIK_ECUDA;
+  if (prop.major != 10 || prop.minor != 0) return LIK_ECUDA;  // built for sm_100a only
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return LIK_ECUDA;
+  lik_ctx* c = new lik_ctx;
+  c->device = cuda_device;
+  c->flags = flags;
+  c->nsm = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return LIK_ECUDA;
+  }
+  *out = c;
+  return LIK_OK;
+}
+
+void lik_destroy(lik_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  cudaFree(c->ws);
+  cudaFree(c->pc);
+  cudaFree(c->bt);
+  cudaFree(c->S);
+  cudaFree(c->io);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+const char* lik_last_error(const lik_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int lik_eval_batch_device(lik_ctx* c, int n, int p, const double* coords, const double* y,
+                          const double* X, int K, const double* params, int M,
+                          const double* lambdas, double* loglik, double* betahat,
+                          double* sigma2hat, double* logdetV, int* status, void* cuda_stream) {
+  if (!c) return LIK_EINVAL;
+  c->err.clear();
+  if (any_null({coords, y, X, params, lambdas, loglik, betahat, sigma2hat, logdetV, status}))
+    return fail(c, LIK_EINVAL, "NULL pointer argument");
+  if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || M + p > 64)
+    return validate(c, n, p, nullptr, nullptr, nullptr, K, M, nullptr);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  std::vector<double> h((size_t)n * (3 + p) + M);
+  double* hc = h.data();
+  double* hy = hc + 2 * (size_t)n;
+  double* hX = hy + n;
+  double* hl = hX + (size_t)n * p;
+  CUDA_TRY(c, cudaMemcpyAsync(hc, coords, 2 * (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(hy, y, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(hX, X, (size_t)n * p * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(hl, lambdas, (size_t)M * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  int rc = validate(c, n, p, hc, hy, hX, K, M, hl);
+  if (rc) return rc;
+  return run_device(c, n, p, coords, y, X, K, params, M, lambdas, loglik, betahat, sigma2hat,
+                    logdetV, status, st);
+}
+
+int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double* y,
+                   const double* X, int K, const double* params, int M, const double* lambdas,
+                   double* loglik, double* betahat, double* sigma2hat, double* logdetV,
+                   int* status) {
+  if (!c) return LIK_EINVAL;
+  c->err.clear();
+  if (any_null({coords, y, X, params, lambdas, loglik, betahat, sigma2hat, logdetV, status}))
+    return fail(c, LIK_EINVAL, "NULL pointer argument");
+  if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || M + p > 64)
+    return validate(c, n, p, nullptr, nullptr, nullptr, K, M, nullptr);
+  int rc = validate(c, n, p, coords, y, X, K, M, lambdas);
+  if (rc) return rc;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = c->own_stream;
+  const size_t in_d = (size_t)n * (3 + p) + (size_t)K * 5 + M;
+  const size_t out_d = (size_t)K * M * (2 + p) + K;
+  const size_t bytes = (in_d + out_d) * 8 + (size_t)K * 4 + 256;
+  if ((rc = ensure(c, &c->io, &c->io_bytes, bytes))) return rc;
+  double* d = reinterpret_cast<double*>(c->io);
+  double* dc = d;
+  double* dy = dc + 2 * (size_t)n;
+  double* dX = dy + n;
+  double* dp = dX + (size_t)n * p;
+  double* dl = dp + (size_t)K * 5;
+  double* dll = dl + M;
+  double* dbh = dll + (size_t)K * M;
+  double* ds2 = dbh + (size_t)K * M * p;
+  double* dld = ds2 + (size_t)K * M;
+  int* dst = reinterpret_cast<int*>(dld + K);
+  CUDA_TRY(c, cudaMemcpyAsync(dc, coords, 2 * (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(dy, y, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(dX, X, (size_t)n * p * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(dp, params, (size_t)K * 5 * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(dl, lambdas, (size_t)M * 8, cudaMemcpyHostToDevice, st));
+  rc = run_device(c, n, p, dc, dy, dX, K, dp, M, dl, dll, dbh, ds2, dld, dst, st);
+  if (rc) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(loglik, dll, (size_t)K * M * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(betahat, dbh, (size_t)K * M * p * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(sigma2hat, ds2, (size_t)K * M * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(logdetV, dld, (size_t)K * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(status, dst, (size_t)K * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  return LIK_OK;
+}
+
+int lik_get_stage_times(lik_ctx* c, double* ms, long long* launches) {
+  if (!c || !(c->flags & LIK_FLAG_TIMING) || !ms || !launches) return LIK_EINVAL;
+  for (int s = 0; s < LIK_NSTAGES; ++s) {
+    ms[s] = c->stage_ms[s];
+    launches[s] = c->stage_n[s];
+  }
+  return LIK_OK;
+}
+
+int lik_reset_stage_times(lik_ctx* c) {
+  if (!c) return LIK_EINVAL;
+  for (int s = 0; s < LIK_NSTAGES; ++s) {
+    c->stage_ms[s] = 0.0;
+    c->stage_n[s] = 0;
+  }
+  return LIK_OK;
+}
+
+int lik_set_wave_points(lik_ctx* c, int pts) {
+  if (!c || pts < 0) return LIK_EINVAL;
+  c->wave_points = pts;
+  return LIK_OK;
+}
+
+int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const double* params,
+                      double* V) {
+  if (!c) return LIK_EINVAL;
+  c->err.clear();
+  if (any_null({coords, params, V})) return fail(c, LIK_EINVAL, "NULL pointer argument");
+  if (n < 1 || K < 1) return fail(c, LIK_EINVAL, "n = %d, K = %d", n, K);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t st = c->own_stream;
+  std::vector<double> hc(2 * (size_t)n);
+  CUDA_TRY(c, cudaMemcpy(hc.data(), coords, 2 * (size_t)n * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(hc[2 * i]) || !std::isfinite(hc[2 * i + 1]))
+      return fail(c, LIK_EINVAL, "coords[%d] is not finite", i);
+  const SlotGeom g = lik::make_geom(n, 0);
+  int rc;
+  if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)K * g.slot_d * sizeof(double)))) return rc;
+  size_t pcb = c->pc_cap * sizeof(PointConst);
+  if ((rc = ensure(c, &c->pc, &pcb, (size_t)K * sizeof(PointConst)))) return rc;
+  c->pc_cap = pcb / sizeof(PointConst);
+  CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
+  CUDA_TRY(c, lik::launch_build(coords, g, c->pc, 0, K, nullptr, c->ws, st));
+  CUDA_TRY(c, lik::launch_unpack_V(g, c->pc, K, c->ws, V, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  return LIK_OK;
+}
+
+}  // extern "C"

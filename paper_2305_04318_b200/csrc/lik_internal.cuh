@@ -1,0 +1,101 @@
+// Internal declarations shared by the liblik.so translation units (product
+// path only; nothing here is shared with the CPU oracle).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lik {
+
+// ---------------------------------------------------------------------------
+// Tile layout of the per-point workspace ("slot") in HBM.
+//
+// The augmented matrix  A = [[V, B], [Bᵀ, 0]]  with B = [y'_1..y'_M | X]
+// (n × r) is stored as 64×64 FP64 tiles: the lower tile-triangle of V
+// (tile (i,j), i ≥ j, index i(i+1)/2 + j) followed by one row of nt
+// "augmented" tiles holding Bᵀ (rows t < r, column block j).  Factoring A by
+// the left-looking Cholesky leaves L (n×n) in the V tiles and Zᵀ = (L⁻¹B)ᵀ in
+// the augmented row, and −BᵀV⁻¹B as the Schur complement of the last block
+// (§3.3 Steps 2-4).
+//
+// Inside a tile the 64 columns are split into two 64×32 "chunks" (16 KB,
+// contiguous), each row-major with an XOR swizzle of the column index so that
+// the DMMA fragment loads from shared memory are bank-conflict free after a
+// 1-D bulk copy (cp.async.bulk) of the chunk.  Because the tiles of one tile
+// row are contiguous, the row panel L[i, 0:j] is one contiguous run of
+// 2j chunks.
+// ---------------------------------------------------------------------------
+constexpr int TB = 64;              // tile edge
+constexpr int KC = 32;              // chunk width (k-extent of one pipeline stage)
+constexpr int TILE_D = TB * TB;     // doubles per tile
+constexpr int CHUNK_D = TB * KC;    // doubles per chunk
+
+__host__ __device__ __forceinline__ int sw_off(int row, int col) {
+  return ((col >> 5) << 11) + (row << 5) + ((col & 31) ^ ((row & 3) << 2));
+}
+__host__ __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
+
+struct SlotGeom {
+  int n;       // sites
+  int nt;      // tiles per dimension = ceil(n / 64)
+  int vlast;   // valid rows of the last tile (1..64)
+  int ntri;    // nt(nt+1)/2
+  int r;       // M + p (augmented rows)
+  int Ra;      // r rounded up to a multiple of 8 (rows copied / computed)
+  size_t slot_d;  // doubles per slot = (ntri + nt) * TILE_D
+};
+
+inline SlotGeom make_geom(int n, int r) {
+  SlotGeom g;
+  g.n = n;
+  g.nt = (n + TB - 1) / TB;
+  g.vlast = n - (g.nt - 1) * TB;
+  g.ntri = g.nt * (g.nt + 1) / 2;
+  g.r = r;
+  g.Ra = (r + 7) & ~7;
+  g.slot_d = (size_t)(g.ntri + g.nt) * TILE_D;
+  return g;
+}
+
+// Per-point constants (one per parameter point), written by setup_kernel.
+enum { MODE_BESSEL = 0, MODE_GAUSS = 1, MODE_BAD = 2 };
+struct PointConst {
+  double cX, sX, sY, cY;   // u/φX = cX hx − sX hy,  v/φY = sY hx + cY hy
+  double kappa, sqrt8k;    // κ, √(8κ)
+  double mu;               // fractional order μ = κ − nl ∈ [−1/2, 1/2)
+  double lnpref;           // (1−κ) ln 2 − ln Γ(κ)
+  double gam1, gam2;       // Temme constants of μ
+  double gampl, gammi;     // 1/Γ(1+μ), 1/Γ(1−μ)
+  double fact;             // πμ / sin(πμ)
+  double nugget;           // ν²
+  int nl;                  // forward-recurrence steps (κ = μ + nl)
+  int mode;                // MODE_*
+};
+
+// Launch wrappers (defined in the .cu files).  All enqueue on `st`.
+cudaError_t launch_prep(const double* y, const double* X, const double* lambdas, int n, int p,
+                        int M, int npad, double* Bt, double* S, cudaStream_t st);
+cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st);
+cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
+                         int kw, const double* Bt, double* ws, cudaStream_t st);
+cudaError_t launch_unpack_V(const SlotGeom& g, const PointConst* pc, int kw, const double* ws,
+                            double* V, cudaStream_t st);
+
+struct CholArgs {
+  double* ws;
+  SlotGeom g;
+  int M, p;
+  const PointConst* pc;
+  int k0;                  // first point of the wave
+  const double* lambdas;   // M
+  const double* S;         // Σ log y (device scalar)
+  double* loglik;          // K×M
+  double* betahat;         // K×M×p
+  double* sigma2hat;       // K×M
+  double* logdetV;         // K
+  int* status;             // K
+};
+cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
+size_t chol_smem_bytes();
+
+}  // namespace lik

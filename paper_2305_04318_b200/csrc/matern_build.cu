@@ -1,0 +1,192 @@
+// Dataset prep (Box-Cox columns, Σ log y), per-point constants, and the
+// Matérn tile build of the augmented matrix [[V, B], [Bᵀ, 0]].
+//   prep_kernel   — a1: y'_m = b(y; λ_m) (R14), Bᵀ rows, S = Σ log y
+//   setup_kernel  — per-point constants of ω_k (R1, R3, R7)
+//   build_kernel  — a2 "matern_build": V = R + ν²I tiles (P:86, P:311 Step 1)
+#include <cfloat>
+#include "bessel_k.cuh"
+#include "lik_internal.cuh"
+
+namespace lik {
+
+// ---------------------------------------------------------------------------
+// prep: grid = r + 1 blocks.  Block t < r writes row t of Bᵀ (r × npad,
+// zero-padded); block r computes S = Σ log y_i with a fixed-order reduction.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ y,
+                                                   const double* __restrict__ X,
+                                                   const double* __restrict__ lambdas, int n,
+                                                   int p, int M, int npad, double* __restrict__ Bt,
+                                                   double* __restrict__ S) {
+  const int t = blockIdx.x;
+  const int r = M + p;
+  if (t < r) {
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+      double v = 0.0;
+      if (i < n) {
+        if (t < M) {
+          const double lam = lambdas[t];
+          const double ly = log(y[i]);
+          v = (fabs(lam) < 1e-10) ? ly : expm1(lam * ly) / lam;
+        } else {
+          v = X[(size_t)i * p + (t - M)];
+        }
+      }
+      Bt[(size_t)t * npad + i] = v;
+    }
+  } else {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) s += log(y[i]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) *S = red[0];
+  }
+}
+
+cudaError_t launch_prep(const double* y, const double* X, const double* lambdas, int n, int p,
+                        int M, int npad, double* Bt, double* S, cudaStream_t st) {
+  prep_kernel<<<M + p + 1, 256, 0, st>>>(y, X, lambdas, n, p, M, npad, Bt, S);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// setup: one thread per parameter point.
+// ---------------------------------------------------------------------------
+__global__ void setup_kernel(const double* __restrict__ params, int K, PointConst* __restrict__ pc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const double phiX = params[5 * (size_t)k + 0], kappa = params[5 * (size_t)k + 1];
+  const double nug = params[5 * (size_t)k + 2], phiR = params[5 * (size_t)k + 3];
+  const double phiA = params[5 * (size_t)k + 4];
+  PointConst P;
+  bool ok = isfinite(phiX) && isfinite(kappa) && isfinite(nug) && isfinite(phiR) &&
+            isfinite(phiA) && phiX > 0.0 && kappa > 0.0 && nug >= 0.0 && phiR > 0.0;
+  P.mode = ok ? (kappa >= 1e3 ? MODE_GAUSS : MODE_BESSEL) : MODE_BAD;
+  double c = 1.0, s = 0.0;
+  if (ok) sincos(phiA, &s, &c);
+  const double phiY = phiX / phiR;  // R3
+  P.cX = c / phiX;
+  P.sX = s / phiX;
+  P.sY = s / phiY;
+  P.cY = c / phiY;
+  P.kappa = kappa;
+  P.sqrt8k = sqrt(8.0 * kappa);
+  P.nugget = nug;
+  int nl = 0;
+  double mu = 0.0;
+  if (P.mode == MODE_BESSEL) {
+    nl = (int)(kappa + 0.5);
+    mu = kappa - nl;
+  }
+  P.nl = nl;
+  P.mu = mu;
+  P.lnpref = ok && P.mode == MODE_BESSEL ? (1.0 - kappa) * 0.69314718055994530942 - lgamma(kappa) : 0.0;
+  temme_constants(mu, &P.gam1, &P.gam2, &P.gampl, &P.gammi, &P.fact);
+  pc[k] = P;
+}
+
+cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st) {
+  setup_kernel<<<(K + 127) / 128, 128, 0, st>>>(params, K, pc);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// build: grid = (ntri + nt tiles, kw points), 256 threads, 16 elements each.
+// Tile (i, j), i ≥ j, of V = R + ν²I (lower tile triangle; the strict upper
+// triangle of a diagonal tile is not referenced by the factorisation and is
+// written as 0).  Padded rows/columns (index ≥ n) hold the identity, which
+// leaves log|V| and L⁻¹B unchanged.  Augmented tile j holds Bᵀ[:, 64j:64j+64].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ coords, SlotGeom g,
+                                                    const PointConst* __restrict__ pc, int k0,
+                                                    const double* __restrict__ Bt,
+                                                    double* __restrict__ ws) {
+  const int tile = blockIdx.x;
+  const int slot = blockIdx.y;
+  const PointConst P = pc[k0 + slot];
+  if (P.mode == MODE_BAD) return;
+  double* T = ws + (size_t)slot * g.slot_d + (size_t)tile * TILE_D;
+  const int npad = g.nt * TB;
+  if (tile >= g.ntri) {
+    const int j = tile - g.ntri;
+    for (int e = threadIdx.x; e < TILE_D; e += 256) {
+      const int r = e >> 6, c = e & 63;
+      T[sw_off(r, c)] = (r < g.r) ? Bt[(size_t)r * npad + j * TB + c] : 0.0;
+    }
+    return;
+  }
+  // tile (i, j) from the packed index
+  int i = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+  while (tri_index(i + 1, 0) <= tile) ++i;
+  while (tri_index(i, 0) > tile) --i;
+  const int j = tile - tri_index(i, 0);
+  __shared__ double sx[2][TB], sy[2][TB];
+  if (threadIdx.x < TB) {
+    const int gi = i * TB + threadIdx.x;
+    sx[0][threadIdx.x] = gi < g.n ? coords[2 * gi] : 0.0;
+    sy[0][threadIdx.x] = gi < g.n ? coords[2 * gi + 1] : 0.0;
+  } else if (threadIdx.x < 2 * TB) {
+    const int gj = j * TB + threadIdx.x - TB;
+    sx[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj] : 0.0;
+    sy[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj + 1] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < TILE_D; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    const int gi = i * TB + r, gj = j * TB + c;
+    double v;
+    if (gi >= g.n || gj >= g.n) {
+      v = (gi == gj) ? 1.0 : 0.0;
+    } else if (gi == gj) {
+      v = 1.0 + P.nugget;
+    } else if (i == j && c > r) {
+      v = 0.0;
+    } else {
+      v = matern_rho(P, sx[0][r] - sx[1][c], sy[0][r] - sy[1][c]);
+    }
+    T[sw_off(r, c)] = v;
+  }
+}
+
+cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
+                         int kw, const double* Bt, double* ws, cudaStream_t st) {
+  dim3 grid(g.ntri + g.nt, kw);
+  build_kernel<<<grid, 256, 0, st>>>(coords, g, pc, k0, Bt, ws);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// unpack (debug / parity only): tiles of V -> dense n×n row-major, mirrored.
+// ---------------------------------------------------------------------------
+__global__ void unpack_V_kernel(SlotGeom g, const PointConst* __restrict__ pc,
+                                const double* __restrict__ ws, double* __restrict__ V) {
+  const int k = blockIdx.y;
+  const size_t nn = (size_t)g.n * g.n;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nn;
+       e += (size_t)gridDim.x * blockDim.x) {
+    int a = (int)(e / g.n), b = (int)(e % g.n);
+    double v;
+    if (pc[k].mode == MODE_BAD) {
+      v = __longlong_as_double(0x7ff8000000000000LL);
+    } else {
+      if (b > a) { int t = a; a = b; b = t; }
+      const int i = a / TB, j = b / TB;
+      v = ws[(size_t)k * g.slot_d + (size_t)tri_index(i, j) * TILE_D + sw_off(a % TB, b % TB)];
+    }
+    V[(size_t)k * nn + e] = v;
+  }
+}
+
+cudaError_t launch_unpack_V(const SlotGeom& g, const PointConst* pc, int kw, const double* ws,
+                            double* V, cudaStream_t st) {
+  dim3 grid(256, kw);
+  unpack_V_kernel<<<grid, 256, 0, st>>>(g, pc, ws, V);
+  return cudaGetLastError();
+}
+
+}  // namespace lik

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs (-m gpu).
+
+Tolerances (north_star / DESIGN.md §6): relative 1e-8 on ℓ_p, σ̂² and log|V|
+(absolute 1e-8 when |log|V|| < 1); max_j |Δβ̂_j| ≤ 1e-8·‖β̂‖∞; V elements
+relative 1e-13 (+ κ and |ln ρ| terms, see test_matern_build_elementwise).  Status codes must agree exactly.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synthgen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2305_04318_b200 as lik  # noqa: E402
+
+NTHREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = lik.create(0)
+    yield c
+    c.close()
+
+
+def assert_parity(gpu, ref, tol=1e-8, label=""):
+    st_g, st_r = gpu["status"], ref["status"]
+    assert np.array_equal(st_g, st_r), f"{label} status mismatch {np.nonzero(st_g != st_r)}"
+    ok = st_r == 0
+    if not ok.any():
+        return
+    ll_g, ll_r = gpu["loglik"][ok], ref["loglik"][ok]
+    rel = np.abs(ll_g - ll_r) / np.abs(ll_r)
+    assert rel.max() <= tol, f"{label} loglik rel {rel.max():.3e} at {np.unravel_index(rel.argmax(), rel.shape)}"
+    s_g, s_r = gpu["sigma2hat"][ok], ref["sigma2hat"][ok]
+    rel = np.abs(s_g - s_r) / np.abs(s_r)
+    assert rel.max() <= tol, f"{label} sigma2 rel {rel.max():.3e}"
+    ld_g, ld_r = gpu["logdetV"][ok], ref["logdetV"][ok]
+    err = np.abs(ld_g - ld_r) / np.maximum(np.abs(ld_r), 1.0)
+    assert err.max() <= tol, f"{label} logdetV err {err.max():.3e}"
+    b_g, b_r = gpu["betahat"][ok], ref["betahat"][ok]
+    scale = np.abs(b_r).max(axis=-1, keepdims=True)
+    err = np.abs(b_g - b_r) / scale
+    assert err.max() <= tol, f"{label} betahat err {err.max():.3e}"
+
+
+def _oracle(orc, coords, y, X, P, lam):
+    return orc.eval_batch(coords, y, X, P, lam, nthreads=NTHREADS)
+
+
+# --------------------------------------------------------------------------- matern_build
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_matern_build_elementwise(ctx, orc, name):
+    coords, y, X, P, lam = synthgen.make_inputs(name, K=64)
+    P = P[:12].copy()
+    P[0, 1] = 100.0     # κ-fixed extremes
+    P[1, 1] = 0.5
+    P[2, 1] = 2000.0    # Gaussian limit (R7)
+    P[3, 1] = 0.21
+    dc = torch.tensor(coords, device="cuda")
+    dp = torch.tensor(P, device="cuda")
+    V = ctx.debug_build_V(dc, dp).cpu().numpy()
+    for k in range(P.shape[0]):
+        ref = orc.build_V(coords, P[k])
+        # ρ = exp(ln ρ) on both sides, so the relative error of ρ is the absolute error
+        # of ln ρ: ~ε·|ln ρ| from the distance and the exponent, plus the cancelling
+        # O(κ ln z) terms of ln(2^{1−κ}/Γ(κ)) + κ ln z + ln K_κ(z).
+        tol = (1e-13 * max(1.0, P[k, 1] / 10.0) if P[k, 1] < 1e3 else 1e-14) \
+            + 2e-15 * np.abs(np.log(np.maximum(ref, 1e-300)))
+        err = np.abs(V[k] - ref) - tol * np.abs(ref)
+        assert err.max() <= 1e-300, (k, P[k], float((np.abs(V[k] - ref) / np.maximum(np.abs(ref), 1e-300)).max()))
+
+
+# --------------------------------------------------------------------------- whole path
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_parity_full_config(ctx, orc, name):
+    coords, y, X, P, lam = synthgen.make_inputs(name)
+    gpu = ctx.eval_batch(coords, y, X, P, lam)
+    ref = _oracle(orc, coords, y, X, P, lam)
+    assert_parity(gpu, ref, label=name)
+
+
+@pytest.mark.parametrize("n,p,M", [(5, 1, 1), (8, 3, 2), (63, 2, 3), (64, 2, 4), (65, 3, 3),
+                                   (127, 4, 5), (129, 1, 7), (191, 5, 11), (250, 2, 30)])
+def test_parity_ragged_sizes(ctx, orc, n, p, M):
+    rng = np.random.default_rng(1000 + n)
+    side = 9000.0 * math.sqrt(n / 224.0)
+    coords = rng.uniform(0, side, size=(n, 2))
+    X = np.column_stack([np.ones(n)] + [rng.normal(size=n) for _ in range(p - 1)])
+    y = np.exp(rng.normal(2.0, 0.4, size=n))
+    cfg = synthgen.Config("R", n, p, 24, M, False, "uniform", "")
+    P = synthgen.make_params(cfg, 24, seed=77 + n)
+    lam = np.linspace(-0.5, 1.2, M)
+    gpu = ctx.eval_batch(coords, y, X, P, lam)
+    ref = _oracle(orc, coords, y, X, P, lam)
+    assert_parity(gpu, ref, label=f"n={n}")
+
+
+def test_parity_C3_subset(ctx, orc):
+    coords, y, X, P, lam = synthgen.make_inputs("C3")
+    sel = np.r_[0:12, np.nonzero(P[:, 1] > 99)[0][:2], np.nonzero(np.isclose(P[:, 1], 0.5))[0][:2]]
+    gpu = ctx.eval_batch(coords, y, X, P[sel], lam)
+    ref = _oracle(orc, coords, y, X, P[sel], lam)
+    assert_parity(gpu, ref, label="C3")
+
+
+def test_parity_C4_bench_launch_sampled(ctx, orc):
+    """Full C4 (K = 20,000, the bench workload and launch configuration) on the
+    GPU; a stratified sample of points recomputed one by one by the oracle."""
+    coords, y, X, P, lam = synthgen.make_inputs("C4")
+    dc, dy, dX, dp, dl = (torch.tensor(a, device="cuda") for a in (coords, y, X, P, lam))
+    out = ctx.eval_batch_device(dc, dy, dX, dp, dl)
+    torch.cuda.synchronize()
+    gpu = {k: v.cpu().numpy() for k, v in out.items()}
+    rng = np.random.default_rng(4)
+    sel = np.unique(np.r_[rng.choice(P.shape[0], 10, replace=False),
+                          np.nonzero(P[:, 1] > 99)[0][:2], np.nonzero(np.isclose(P[:, 1], 0.5))[0][:1],
+                          [0, P.shape[0] - 1]])
+    ref = _oracle(orc, coords, y, X, P[sel], lam)
+    assert_parity({k: v[sel] for k, v in gpu.items()}, ref, label="C4")
+    assert np.all(gpu["status"] == 0)
+    assert np.all(np.isfinite(gpu["loglik"]))
+
+
+# --------------------------------------------------------------------------- edge cases
+def test_status_codes(ctx, orc):
+    coords, y, X = synthgen.make_dataset("C1")
+    good = [900.0, 1.5, 0.2, 1.0, 0.0]
+    P = np.array([good, [-1.0, 1.5, 0.2, 1.0, 0.0], [900.0, 0.0, 0.2, 1.0, 0.0],
+                  [900.0, 1.5, -0.1, 1.0, 0.0], [900.0, 1.5, 0.2, 0.0, 0.0],
+                  [900.0, float("nan"), 0.2, 1.0, 0.0], [900.0, float("inf"), 0.2, 1.0, 0.0], good])
+    gpu = ctx.eval_batch(coords, y, X, P, [0.3, 0.7])
+    ref = _oracle(orc, coords, y, X, P, [0.3, 0.7])
+    assert list(gpu["status"]) == [0, 4, 4, 4, 4, 4, 4, 0]
+    assert_parity(gpu, ref)
+    assert np.all(np.isneginf(gpu["loglik"][1:7])) and np.all(np.isnan(gpu["logdetV"][1:7]))
+    assert np.all(np.isnan(gpu["betahat"][1:7]))
+    # V not PD (dense sites, long smooth range, no nugget): both sides flag it
+    c2 = np.stack([np.arange(70) * 1.0, np.zeros(70)], axis=1)
+    y2 = 1.0 + np.arange(70.0)
+    P2 = [[1e5, 10.0, 0.0, 1.0, 0.0], [5.0, 0.5, 0.1, 1.0, 0.0]]
+    g2 = ctx.eval_batch(c2, y2, np.ones((70, 1)), P2, [0.5])
+    r2 = _oracle(orc, c2, y2, np.ones((70, 1)), P2, [0.5])
+    assert g2["status"][0] == 1 and r2["status"][0] == 1
+    assert_parity(g2, r2)
+
+
+def test_call_level_errors(ctx):
+    coords, y, X = synthgen.make_dataset("C1")
+    P = [[900.0, 1.5, 0.2, 1.0, 0.0]]
+    assert ctx.eval_batch_rc(coords, y, X, P, [0.5])[0] == lik.LIK_OK
+    y2 = y.copy()
+    y2[7] = -1.0
+    rc, msg = ctx.eval_batch_rc(coords, y2, X, P, [0.5])
+    assert rc == lik.LIK_EDOMAIN and "y[7]" in msg
+    c3 = coords.copy()
+    c3[9] = c3[4]
+    rc, msg = ctx.eval_batch_rc(c3, y, X, P, [0.5])
+    assert rc == lik.LIK_EDOMAIN and "4" in msg and "9" in msg
+    rc, _ = ctx.eval_batch_rc(coords, y, np.column_stack([X, 2 * X[:, 1]]), P, [0.5])
+    assert rc == lik.LIK_ERANK
+    rc, _ = ctx.eval_batch_rc(coords[:3], y[:3], X[:3], P, [0.5])
+    assert rc == lik.LIK_EINVAL
+    rc, _ = ctx.eval_batch_rc(coords, y, X, P, np.linspace(0, 1, 63))
+    assert rc == lik.LIK_EINVAL
+    c4 = coords.copy()
+    c4[3, 0] = float("nan")
+    assert ctx.eval_batch_rc(c4, y, X, P, [0.5])[0] == lik.LIK_EINVAL
+
+
+def test_wide_r_and_gaussian_limit(ctx, orc):
+    # M + p = 64 (the ABI maximum) and κ ≥ 1e3 (Gaussian limit, R7)
+    coords, y, X = synthgen.make_dataset("C1")
+    lam = np.linspace(-1.0, 1.5, 62)
+    P = np.array([[900.0, 1.5, 0.2, 1.0, 0.0], [600.0, 3000.0, 0.3, 1.0, 0.0]])
+    assert_parity(ctx.eval_batch(coords, y, X, P, lam), _oracle(orc, coords, y, X, P, lam))
+
+
+def test_determinism_waves_and_apis(ctx):
+    coords, y, X, P, lam = synthgen.make_inputs("C2", K=300)
+    a = ctx.eval_batch(coords, y, X, P, lam)
+    for w in (1, 7, 64):
+        ctx.set_wave_points(w)
+        b = ctx.eval_batch(coords, y, X, P, lam)
+        for key in a:
+            assert np.array_equal(a[key], b[key], equal_nan=True), (w, key)
+    ctx.set_wave_points(0)
+    # permuting points permutes outputs bitwise
+    perm = np.random.default_rng(2).permutation(P.shape[0])
+    c = ctx.eval_batch(coords, y, X, P[perm], lam)
+    for key in a:
+        assert np.array_equal(a[key][perm], c[key], equal_nan=True)
+    # device API on torch tensors, on a side stream
+    dc, dy, dX, dp, dl = (torch.tensor(v, device="cuda") for v in (coords, y, X, P, lam))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        out = ctx.eval_batch_device(dc, dy, dX, dp, dl, stream=s)
+    s.synchronize()
+    for key in a:
+        assert np.array_equal(a[key], out[key].cpu().numpy(), equal_nan=True), key
+
+
+def test_stage_timing_api():
+    c = lik.create(0, lik.FLAG_TIMING)
+    coords, y, X, P, lam = synthgen.make_inputs("C2", K=200)
+    c.eval_batch(coords, y, X, P, lam)
+    t = c.stage_times()
+    assert t["chol_fused"][1] >= 1 and t["chol_fused"][0] > 0
+    assert t["matern_build"][1] == t["chol_fused"][1]
+    c.reset_stage_times()
+    assert c.stage_times()["chol_fused"] == (0.0, 0)
+    c.close()
