@@ -1,0 +1,317 @@
+"""Benchmark of the hot path: profile-likelihood parameter points per second at
+n = 2000 (BASELINE.json configs[3], "C4"), FP64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+A "step" is one lik_eval_batch_device call over the whole per-rank batch of
+K_pts = 20,000 parameter points × 5 Box-Cox λ (all of SURVEY §8(a): prep,
+matern_build, Cholesky, solve, cross products, epilogue), inputs resident in
+HBM.  Multi-GPU is weak scaling: every rank evaluates its own 20,000 points
+(points sharded k ≡ rank mod N from one N·20,000-point set) and the result
+tables are all-gathered over NCCL (the one exchange step).  `value` = all
+points processed ÷ max-over-ranks device time.  The L2 (126 MB) is flushed
+with a 256 MiB write before every timed step.
+
+`e2e` is the same metric through the host-pointer ABI call lik_eval_batch:
+host→device copy of the step's inputs from pinned memory, the path, and the
+device→host copy of the outputs, all inside the timed region.
+
+`--impl reference` times the CPU oracle (oracle/, the parity reference) on the
+host cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthgen  # noqa: E402
+
+WORKLOAD = "C4"
+METRIC = "profile-likelihood param points/sec at n=2000 (1/2/4/8 B200); FP64 TFLOP/s vs peak"
+UNIT = "points/s"
+PHASE0 = os.path.join(ROOT, "profiles", "r01", "phase0_fp64_peaks.jsonl")
+TRAFFIC = os.path.join(ROOT, "profiles", "chol_traffic.json")
+
+
+def dense_flops_per_point(n, r):
+    """algorithmic FP64 flops per point = n³/3 + n²r + n r²."""
+    return n ** 3 / 3.0 + n * n * r + n * r * r
+
+
+def fp64_peak():
+    """Measured DMMA.8x8x4 FP64 peak (tools/phase0, TFLOP/s) else 37.2 nominal."""
+    try:
+        vals = [json.loads(l) for l in open(PHASE0)]
+        best = max(v["tflops"] for v in vals if v.get("kind") == "dmma_sustained")
+        return best, "measured: DMMA.8x8x4 loop, tools/phase0 (profiles/r01/phase0_fp64_peaks.jsonl)"
+    except Exception:
+        return 37.2, "nominal: 148 SM x 64 FMA/clk x 2 x 1.965 GHz"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(coords, y, X, P, lam, budget_s=20.0):
+    """The oracle, as it stands, on the host cores over a bounded sample of points."""
+    import oracle
+    T = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.eval_batch(coords, y, X, P[:T], lam, nthreads=T)  # one point per thread
+    t1 = time.perf_counter()
+    per_round = t1 - t0
+    rounds = max(1, min(4, int(budget_s / max(per_round, 1e-3)) - 1))
+    npts = T
+    tt = per_round
+    if rounds > 1:
+        t0 = time.perf_counter()
+        oracle.eval_batch(coords, y, X, P[T:T * rounds], lam, nthreads=T)
+        tt += time.perf_counter() - t0
+        npts += T * (rounds - 1)
+    return {"value": npts / tt, "unit": UNIT, "cores": T, "kind": "oracle",
+            "sample": f"{npts} points of {WORKLOAD} (n=2000, p=5, M=5) over {T} threads, {tt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle timed on the box's host cores."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cfg = synthgen.CONFIGS[WORKLOAD]
+    coords, y, X = synthgen.make_dataset(cfg)
+    P = synthgen.make_params(cfg)
+    lam = synthgen.make_lambdas(cfg.M)
+    T = os.cpu_count() or 1
+    pts_per_step = T  # one C4 point per host thread per step (~3 s of CPU each)
+    for w in range(args.warmup):
+        oracle.eval_batch(coords, y, X, P[w * T:(w + 1) * T][:1], lam, nthreads=1)
+    times = []
+    for s in range(args.steps):
+        sl = P[(s * pts_per_step) % cfg.K:][:pts_per_step]
+        t0 = time.perf_counter()
+        oracle.eval_batch(coords, y, X, sl, lam, nthreads=T)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = pts_per_step / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{WORKLOAD}: {cfg.desc}", "n": cfg.n, "p": cfg.p, "M": cfg.M,
+                       "K_per_step": pts_per_step, "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle",
+                             "sample": f"{pts_per_step} points of {WORKLOAD} per step, {T} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--points", type=int, default=None, help="points per rank (default 20000)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_04318_b200 as lik
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = synthgen.CONFIGS[WORKLOAD]
+    K = args.points or cfg.K
+    coords, y, X = synthgen.make_dataset(cfg)
+    Pall = synthgen.make_params(cfg, K * world)
+    P = np.ascontiguousarray(Pall[rank::world])  # strided sharding balances κ-dependent cost
+    lam = synthgen.make_lambdas(cfg.M)
+    n, p, M = cfg.n, cfg.p, cfg.M
+    r = M + p
+
+    ctx = lik.create(local, lik.FLAG_TIMING)
+    st = torch.cuda.Stream(dev)
+    dc, dy, dX, dp, dl = (torch.tensor(a, device=dev) for a in (coords, y, X, P, lam))
+    out = lik.Ctx.alloc_outputs(K, M, p, dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    pack_w = M * (2 + p) + 2
+    gathered = torch.empty((world, K, pack_w), dtype=torch.float64, device=dev) if world > 1 else None
+
+    def step():
+        ctx.eval_batch_device(dc, dy, dX, dp, dl, out=out, stream=st)
+        if world > 1:
+            with torch.cuda.stream(st):
+                packed = torch.cat([out["loglik"], out["sigma2hat"], out["betahat"].reshape(K, -1),
+                                    out["logdetV"][:, None], out["status"][:, None].double()], 1)
+                dist.all_gather_into_tensor(gathered.view(world * K, pack_w), packed)
+
+    for _ in range(args.warmup):
+        with torch.cuda.stream(st):
+            flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    ctx.reset_stage_times()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for s in range(args.steps):
+            with torch.cuda.stream(st):
+                flush.fill_(float(s))
+            evs[s][0].record(st)
+            step()
+            evs[s][1].record(st)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_local = float(np.mean(step_ms))
+    stages = ctx.stage_times()
+    # max over ranks
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_pts = K * world
+    value = total_pts / (ms / 1e3)
+    F = dense_flops_per_point(n, r)
+    ok_frac = float((out["status"] == 0).float().mean().item())
+
+    # ---- e2e through the host-pointer ABI (pinned host inputs, copies inside the timed region)
+    hin = [torch.tensor(a).pin_memory() for a in (coords, y, X, P, lam)]
+    hn = [h.numpy() for h in hin]
+    e2e_ctx = lik.create(local)
+    e2e_ctx.eval_batch(*hn)  # warm (allocations)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_steps = max(1, min(args.steps, 2))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = e2e_ctx.eval_batch(*hn)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = total_pts / float(te.item())
+    h2d = sum(a.nbytes for a in hn)
+    d2h = sum(v.nbytes for v in res.values())
+    e2e_ctx.close()
+
+    if rank == 0:
+        chol_ms, chol_n = stages["chol_fused"]
+        build_ms, build_n = stages["matern_build"]
+        peak, peak_src = fp64_peak()
+        achieved = (args.steps * K * F) / (chol_ms / 1e3) / 1e12 if chol_ms > 0 else None
+        traffic = None
+        try:
+            traffic = json.load(open(TRAFFIC)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{WORKLOAD}: {cfg.desc}", "n": n, "p": p, "M": M,
+                       "K_per_rank": K, "parallelism": f"points sharded over {world} GPU(s)",
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "wall_s_timed_region": round(t_wall, 3)},
+            "fp64_tflops": value * F / 1e12,
+            "fp64_tflops_per_gpu": value * F / 1e12 / world,
+            "roofline": {"bound": "tensor", "kernel": "chol_fused (DMMA.8x8x4)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "algorithmic": "n^3/3 + n^2 r + n r^2 FP64 flops per point (SURVEY §8(d)), "
+                                        "x points per launch / launch duration (CUDA events on the launching stream)",
+                         "share_of_step": chol_ms / (args.steps * ms_local) if ms_local else None},
+            "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
+            "gpu_launches": int(sum(v[1] for v in stages.values())),
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "status_ok_fraction": ok_frac,
+            "input_hash": synthgen.input_hash(coords, y, X, P, lam),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(coords, y, X, P, lam)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -76,7 +76,7 @@ enum {
 enum {
   LIK_STAGE_PREP = 0,   /* Box-Cox columns, Σ log y (a1) */
   LIK_STAGE_SETUP = 1,  /* per-point constants (a2 prologue) */
-  LIK_STAGE_BUILD = 2,  /* matern_build: V tiles + [y'|X]ᵀ rows (a2) */
+  LIK_STAGE_BUILD = 2,  /* matern_build: ln ρ Chebyshev table + V tiles + [y'|X]ᵀ rows (a2) */
   LIK_STAGE_CHOL = 3,   /* chol_fused: Cholesky, solve, cross products, epilogue (a3-a7) */
   LIK_NSTAGES = 4
 };

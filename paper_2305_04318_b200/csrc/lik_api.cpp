@@ -30,6 +30,8 @@ struct lik_ctx {
   double* bt = nullptr;
   size_t bt_bytes = 0;
   double* S = nullptr;
+  double* table = nullptr;
+  size_t table_bytes = 0;
   // host-API staging buffers
   char* io = nullptr;
   size_t io_bytes = 0;
@@ -160,6 +162,8 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   if ((rc = ensure(c, &c->bt, &c->bt_bytes, (size_t)g.r * g.nt * lik::TB * sizeof(double) + 64)))
     return rc;
   if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, sizeof(double)));
+  if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)W * lik::TABLE_D * sizeof(double))))
+    return rc;
 
   const bool timing = c->flags & LIK_FLAG_TIMING;
   const int nwaves = (K + W - 1) / W;
@@ -171,7 +175,8 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   for (int w = 0; w < nwaves; ++w) {
     const int k0 = w * W, kw = std::min(W, K - k0);
-    CUDA_TRY(c, lik::launch_build(coords, g, c->pc, k0, kw, c->bt, c->ws, st));
+    CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, st));
+    CUDA_TRY(c, lik::launch_build(coords, g, c->pc, k0, kw, c->table, c->bt, c->ws, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
     a.ws = c->ws;
@@ -205,7 +210,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
       cudaEventElapsedTime(&ms, c->ev[3 + 2 * w], c->ev[4 + 2 * w]);
       c->stage_ms[LIK_STAGE_CHOL] += ms;
     }
-    c->stage_n[LIK_STAGE_BUILD] += nwaves;
+    c->stage_n[LIK_STAGE_BUILD] += 2 * nwaves;  // table + build
     c->stage_n[LIK_STAGE_CHOL] += nwaves;
   }
   return LIK_OK;
@@ -252,6 +257,7 @@ void lik_destroy(lik_ctx* c) {
   cudaFree(c->pc);
   cudaFree(c->bt);
   cudaFree(c->S);
+  cudaFree(c->table);
   cudaFree(c->io);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -376,8 +382,11 @@ int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const doub
   size_t pcb = c->pc_cap * sizeof(PointConst);
   if ((rc = ensure(c, &c->pc, &pcb, (size_t)K * sizeof(PointConst)))) return rc;
   c->pc_cap = pcb / sizeof(PointConst);
+  if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)K * lik::TABLE_D * sizeof(double))))
+    return rc;
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
-  CUDA_TRY(c, lik::launch_build(coords, g, c->pc, 0, K, nullptr, c->ws, st));
+  CUDA_TRY(c, lik::launch_table(c->pc, 0, K, c->table, st));
+  CUDA_TRY(c, lik::launch_build(coords, g, c->pc, 0, K, c->table, nullptr, c->ws, st));
   CUDA_TRY(c, lik::launch_unpack_V(g, c->pc, K, c->ws, V, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
   return LIK_OK;

@@ -70,14 +70,28 @@ struct PointConst {
   double nugget;           // ν²
   int nl;                  // forward-recurrence steps (κ = μ + nl)
   int mode;                // MODE_*
+  int e_zero;              // ρ ≡ 0 (ln ρ < −750) for z ≥ 2^e_zero (set by table_kernel)
 };
+
+// Per-point Chebyshev table of ln ρ(z) on binary octaves z ∈ [2^e, 2^{e+1}),
+// e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1.  Each octave stores CHEB_STRIDE
+// doubles: a base H_o followed by CHEB_N Chebyshev coefficients of
+// h(z) = ln ρ(z) + z − H_o, so that ln ρ = (H_o + h(z)) − z.  Below 2^CHEB_ELO
+// the exact evaluation is used; at and above 2^e_zero ρ = 0.
+constexpr int CHEB_N = 20;
+constexpr int CHEB_STRIDE = CHEB_N + 1;
+constexpr int CHEB_ELO = -26;
+constexpr int CHEB_NOCT = 40;
+constexpr int TABLE_D = CHEB_STRIDE * CHEB_NOCT;
 
 // Launch wrappers (defined in the .cu files).  All enqueue on `st`.
 cudaError_t launch_prep(const double* y, const double* X, const double* lambdas, int n, int p,
                         int M, int npad, double* Bt, double* S, cudaStream_t st);
 cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st);
+cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, cudaStream_t st);
 cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
-                         int kw, const double* Bt, double* ws, cudaStream_t st);
+                         int kw, const double* table, const double* Bt, double* ws,
+                         cudaStream_t st);
 cudaError_t launch_unpack_V(const SlotGeom& g, const PointConst* pc, int kw, const double* ws,
                             double* V, cudaStream_t st);
 

@@ -85,6 +85,7 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
   }
   P.nl = nl;
   P.mu = mu;
+  P.e_zero = 1 << 20;  // set by table_kernel
   P.lnpref = ok && P.mode == MODE_BESSEL ? (1.0 - kappa) * 0.69314718055994530942 - lgamma(kappa) : 0.0;
   temme_constants(mu, &P.gam1, &P.gam2, &P.gampl, &P.gammi, &P.fact);
   pc[k] = P;
@@ -92,6 +93,72 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
 
 cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st) {
   setup_kernel<<<(K + 127) / 128, 128, 0, st>>>(params, K, pc);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// table: one block per point of the wave.  ln ρ is evaluated exactly (Temme /
+// CF2 + recurrence) at CHEB_N Chebyshev nodes of every binary octave of z below
+// the underflow octave e_zero, and turned into Chebyshev coefficients (DCT-II).
+// ln ρ(z) is analytic on each octave [a, 2a] (its only finite singularity is the
+// branch point z = 0, three half-widths from the centre), so degree 19 reaches
+// the FP64 rounding floor (~1e-16·max(1, |ln ρ|)), DESIGN.md §5.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc, int k0,
+                                                    double* __restrict__ table) {
+  const int k = k0 + blockIdx.x;
+  const int tid = threadIdx.x;
+  const PointConst P = pc[k];
+  if (P.mode != MODE_BESSEL) return;
+  __shared__ double f[CHEB_NOCT * CHEB_N];
+  __shared__ double edge[CHEB_NOCT + 1];
+  __shared__ int ez;
+  for (int o = tid; o <= CHEB_NOCT; o += 256) edge[o] = log_rho_exact(P, ldexp(1.0, CHEB_ELO + o));
+  __syncthreads();
+  if (tid == 0) {
+    int e0 = CHEB_ELO + CHEB_NOCT + 64;  // sentinel: never underflows inside the table range
+    for (int o = 0; o <= CHEB_NOCT; ++o)
+      if (edge[o] < -750.0) {
+        e0 = CHEB_ELO + o;
+        break;
+      }
+    ez = e0;
+    pc[k].e_zero = e0;
+  }
+  __syncthreads();
+  // g(z) = ln ρ(z) + z at the nodes (the −z trend of ln ρ removed)
+  for (int idx = tid; idx < CHEB_NOCT * CHEB_N; idx += 256) {
+    const int o = idx / CHEB_N, i = idx % CHEB_N;
+    const int e = CHEB_ELO + o;
+    double v = 0.0;
+    if (e < ez) {
+      const double x = cospi((i + 0.5) / CHEB_N);
+      const double z = ldexp(1.5 + 0.5 * x, e);
+      v = log_rho_exact(P, z) + z;
+    }
+    f[idx] = v;
+  }
+  __syncthreads();
+  // per octave: base H_o = g at the middle node, coefficients of g − H_o (DCT-II)
+  double* T = table + (size_t)blockIdx.x * TABLE_D;
+  for (int idx = tid; idx < CHEB_NOCT * CHEB_STRIDE; idx += 256) {
+    const int o = idx / CHEB_STRIDE, j = idx % CHEB_STRIDE - 1;
+    double c = 0.0;
+    if (CHEB_ELO + o < ez) {
+      const double H = f[o * CHEB_N + CHEB_N / 2];
+      if (j < 0) {
+        c = H;
+      } else {
+        for (int i = 0; i < CHEB_N; ++i) c += (f[o * CHEB_N + i] - H) * cospi(j * (i + 0.5) / CHEB_N);
+        c *= (j == 0 ? 1.0 : 2.0) / CHEB_N;
+      }
+    }
+    T[idx] = c;
+  }
+}
+
+cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, cudaStream_t st) {
+  table_kernel<<<kw, 256, 0, st>>>(pc, k0, table);
   return cudaGetLastError();
 }
 
@@ -104,6 +171,7 @@ cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ coords, SlotGeom g,
                                                     const PointConst* __restrict__ pc, int k0,
+                                                    const double* __restrict__ table,
                                                     const double* __restrict__ Bt,
                                                     double* __restrict__ ws) {
   const int tile = blockIdx.x;
@@ -126,6 +194,12 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
   while (tri_index(i, 0) > tile) --i;
   const int j = tile - tri_index(i, 0);
   __shared__ double sx[2][TB], sy[2][TB];
+  __shared__ double coef[TABLE_D];
+  if (P.mode == MODE_BESSEL) {
+    const double* src = table + (size_t)slot * TABLE_D;
+    const int nval = min(CHEB_NOCT, max(0, P.e_zero - CHEB_ELO)) * CHEB_STRIDE;
+    for (int e = threadIdx.x; e < nval; e += 256) coef[e] = src[e];
+  }
   if (threadIdx.x < TB) {
     const int gi = i * TB + threadIdx.x;
     sx[0][threadIdx.x] = gi < g.n ? coords[2 * gi] : 0.0;
@@ -147,16 +221,17 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
     } else if (i == j && c > r) {
       v = 0.0;
     } else {
-      v = matern_rho(P, sx[0][r] - sx[1][c], sy[0][r] - sy[1][c]);
+      v = matern_rho_table(P, coef, sx[0][r] - sx[1][c], sy[0][r] - sy[1][c]);
     }
     T[sw_off(r, c)] = v;
   }
 }
 
 cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
-                         int kw, const double* Bt, double* ws, cudaStream_t st) {
+                         int kw, const double* table, const double* Bt, double* ws,
+                         cudaStream_t st) {
   dim3 grid(g.ntri + g.nt, kw);
-  build_kernel<<<grid, 256, 0, st>>>(coords, g, pc, k0, Bt, ws);
+  build_kernel<<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
   return cudaGetLastError();
 }
 
