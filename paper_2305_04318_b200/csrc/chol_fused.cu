@@ -9,14 +9,18 @@
 //             L_jj⁻¹ for the solves of this column
 //     i > j:  L_ij = C L_jj⁻ᵀ                   (DMMA)
 // The augmented row ends up holding Zᵀ = (L⁻¹B)ᵀ (Step 3), and its final
-// diagonal block  −Σ_k Z_k Z_kᵀ = −BᵀV⁻¹B  is the cross-product matrix ssqYX of
+// diagonal block  Σ_k Z_k Z_kᵀ = BᵀV⁻¹B  is the cross-product matrix ssqYX of
 // Table 1 (Step 4).  The epilogue does Steps 5-8 and Eq. (profile).
 //
-// Operand staging: tiles are stored as contiguous 64×32 swizzled chunks
+// Operand staging: tiles are stored as contiguous 64×16 swizzled chunks
 // (lik_internal.cuh), so each pipeline stage is three 1-D bulk copies
 // (cp.async.bulk, the TMA engine) completing on an mbarrier; a 3-stage ring.
+// The L_j panel (B operand, reused by every row block of column j) is loaded
+// with an L2 evict_last policy, the streamed A panels with evict_first.
 // 256 threads = 8 warps as 4 (32-row) × 2 (32-column) warp tiles of a 128×64
-// row block; each warp owns 4×4 DMMA 8×8 accumulators.
+// row block; each warp owns 4×4 DMMA 8×8 accumulators.  Two CTAs per SM
+// (≤ 128 registers, ~105 KB shared memory each), so the serial phases of one
+// point (diagonal factorisation, inverse) overlap the DMMA phases of the other.
 #include <cfloat>
 #include <cstdint>
 #include "../../include/lik.h"
@@ -27,12 +31,14 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int NSTAGE = 3;
-constexpr int STAGE_D = 3 * CHUNK_D;  // A rows of tile a, A rows of tile b, B rows
+constexpr int STAGE_D = 3 * CHUNK_D;             // A rows of tile a, A rows of tile b, B rows
+constexpr int OFF_SCRATCH = 2 * TILE_D;          // 32×32 scratch after the staging tiles
 constexpr int OFF_LINV = NSTAGE * STAGE_D;
 constexpr int OFF_DLOG = OFF_LINV + TILE_D;
 constexpr int OFF_MISC = OFF_DLOG + 64;          // 8 doubles of scalars
 constexpr int OFF_MBAR = OFF_MISC + 8;           // NSTAGE uint64
 constexpr int SMEM_D = OFF_MBAR + NSTAGE + 4;    // + int flags
+static_assert(OFF_SCRATCH + 32 * 32 <= OFF_LINV, "staging + scratch must fit in the stage ring");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -62,11 +68,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
         : "memory");
   }
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
+                                         uint32_t bar, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
@@ -75,40 +92,58 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 typedef double Acc[4][4][2];
 
-// One 64×32 chunk (8 k-steps of 4) of  acc += A_rows · B_rowsᵀ  for this warp.
+// One 64×16 chunk (4 k-steps of 4) of  acc += A_rows · B_rowsᵀ  for this warp.
+// MFULL: all four 8-row subtiles of the warp are live (the common case), so the
+// DMMA sequence is branch- and predicate-free.
+template <bool MFULL>
 __device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ Ab, int rbase,
                                           int mlim, const double* __restrict__ Bb, int cbase,
                                           int lane) {
   const int lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
+  for (int kk = 0; kk < KC / 4; ++kk) {
     const int kcol = ((kk * 4) ^ sw) + lc;
     double a[4], b[4];
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) b[ni] = Bb[(cbase + ni * 8 + lr) * KC + kcol];
+    if (MFULL) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-      if (mi < mlim) {
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
-      }
+    } else {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+        if (mi < mlim) {
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        }
+    }
   }
 }
 
-__device__ __forceinline__ void frag_load(Acc& acc, const double* __restrict__ T, int rbase,
-                                          int cbase, int mlim, int lane) {
+__device__ __forceinline__ void mma_chunk_any(Acc& acc, const double* Ab, int rbase, int mlim,
+                                              const double* Bb, int cbase, int lane) {
+  if (mlim == 4)
+    mma_chunk<true>(acc, Ab, rbase, 4, Bb, cbase, lane);
+  else if (mlim > 0)
+    mma_chunk<false>(acc, Ab, rbase, mlim, Bb, cbase, lane);
+}
+
+__device__ __forceinline__ void frag_load_neg(Acc& acc, const double* __restrict__ T, int rbase,
+                                              int cbase, int mlim, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
       if (mi < mlim) {
-        const double2 v =
-            *reinterpret_cast<const double2*>(T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc));
-        acc[mi][ni][0] = v.x;
-        acc[mi][ni][1] = v.y;
+        const double2 v = *reinterpret_cast<const double2*>(
+            T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc));
+        acc[mi][ni][0] = -v.x;
+        acc[mi][ni][1] = -v.y;
       } else {
         acc[mi][ni][0] = 0.0;
         acc[mi][ni][1] = 0.0;
@@ -116,6 +151,7 @@ __device__ __forceinline__ void frag_load(Acc& acc, const double* __restrict__ T
     }
 }
 
+template <bool NEG>
 __device__ __forceinline__ void frag_store(const Acc& acc, double* __restrict__ T, int rbase,
                                            int cbase, int mlim, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
@@ -125,8 +161,8 @@ __device__ __forceinline__ void frag_store(const Acc& acc, double* __restrict__ 
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
         double2 v;
-        v.x = acc[mi][ni][0];
-        v.y = acc[mi][ni][1];
+        v.x = NEG ? -acc[mi][ni][0] : acc[mi][ni][0];
+        v.y = NEG ? -acc[mi][ni][1] : acc[mi][ni][1];
         *reinterpret_cast<double2*>(T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc)) = v;
       }
     }
@@ -143,12 +179,12 @@ struct Pipe {
   double* stages;
   uint64_t* mbar;
   uint32_t seq;  // chunks consumed so far (same value in every thread)
+  uint64_t pol_stream, pol_keep;
 };
 
-// acc -= (or +=) Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
+// acc += Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
 //   A rows of tile a: gA0 + q·CHUNK_D (cA0 rows copied), tile b: gA1 (cA1 rows),
-//   B rows: gB (cB rows).  The accumulation sign is folded in by the caller
-//   (acc starts at −A_ij and the result is negated) — here acc += A Bᵀ.
+//   B rows: gB (cB rows).
 __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int cA0,
                                       const double* gA1, int cA1, const double* gB, int cB,
                                       int nq, bool mine_b, int rbase, int mlim, int cbase,
@@ -160,9 +196,10 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int
     double* st = pp.stages + s * STAGE_D;
     const uint32_t bar = saddr(&pp.mbar[s]);
     mbar_expect_tx(bar, (uint32_t)(cA0 + cA1 + cB) * KC * 8);
-    bulk_g2s(saddr(st), gA0 + (size_t)q * CHUNK_D, cA0 * KC * 8, bar);
-    if (cA1) bulk_g2s(saddr(st + CHUNK_D), gA1 + (size_t)q * CHUNK_D, cA1 * KC * 8, bar);
-    bulk_g2s(saddr(st + 2 * CHUNK_D), gB + (size_t)q * CHUNK_D, cB * KC * 8, bar);
+    bulk_g2s(saddr(st), gA0 + (size_t)q * CHUNK_D, cA0 * KC * 8, bar, pp.pol_stream);
+    if (cA1)
+      bulk_g2s(saddr(st + CHUNK_D), gA1 + (size_t)q * CHUNK_D, cA1 * KC * 8, bar, pp.pol_stream);
+    bulk_g2s(saddr(st + 2 * CHUNK_D), gB + (size_t)q * CHUNK_D, cB * KC * 8, bar, pp.pol_keep);
   };
   if (tid == 0) {
     issue(0);
@@ -173,16 +210,16 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int
     const uint32_t s = (seq + q) % NSTAGE;
     mbar_wait(saddr(&pp.mbar[s]), ((seq + q) / NSTAGE) & 1);
     const double* st = pp.stages + s * STAGE_D;
-    if (mlim > 0) mma_chunk(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, cbase, lane);
+    mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, cbase, lane);
     __syncthreads();
   }
   pp.seq = seq + nq;
 }
 
 // Unblocked Cholesky of the leading v×v block of a 64×64 tile in shared memory
-// (lower part used; rows/columns ≥ v are the identity padding and are never
-// read).  dlog[c] = log(pivot_c) = 2 log L_cc.  Returns nonzero (uniformly) if
-// a pivot is ≤ tol (R11).
+// (lower part used).  dlog[c] = log(pivot_c) = 2 log L_cc.  Returns nonzero
+// (uniformly) if a pivot is ≤ tol (R11).  Afterwards rows/columns ≥ v are set
+// to the identity (the padding of V), so the tile is a complete 64×64 factor.
 __device__ int potrf64(double* S, int v, double tol, double* dlog, double* scal, int* flag) {
   const int tid = threadIdx.x;
   for (int c = 0; c < v; ++c) {
@@ -208,28 +245,50 @@ __device__ int potrf64(double* S, int v, double tol, double* dlog, double* scal,
     }
     __syncthreads();
   }
+  if (v < TB) {
+    for (int e = tid; e < TILE_D; e += NT) {
+      const int rr = e >> 6, kk = e & 63;
+      if (rr >= v && kk <= rr) S[sw_off(rr, kk)] = (rr == kk) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+  }
   return 0;
 }
 
-// X = L⁻¹ for the leading v×v block (column-wise forward substitution); the
-// padded block of X is the identity, so the solves leave padded columns of the
-// right-hand side (which are zero) unchanged.
-__device__ void trinv64(const double* S, int v, double* X) {
-  const int c = threadIdx.x;
-  if (c < TB) {
-    for (int i = 0; i < TB; ++i) {
-      double x;
-      if (i < c) {
-        x = 0.0;
-      } else if (c >= v || i >= v) {
-        x = (i == c) ? 1.0 : 0.0;
-      } else {
-        double s = (i == c) ? 1.0 : 0.0;
-        for (int k = c; k < i; ++k) s -= S[sw_off(i, k)] * X[sw_off(k, c)];
-        x = s / S[sw_off(i, i)];
+// X = L⁻¹ (64×64 lower triangular) in two levels of 32×32 blocks:
+//   X11 = L11⁻¹, X22 = L22⁻¹ (column-parallel forward substitution, 64 threads),
+//   X21 = −X22 (L21 X11)  (all threads; T = L21 X11 in the 32×32 scratch).
+__device__ void trinv64(const double* S, double* X, double* T) {
+  const int tid = threadIdx.x;
+  if (tid < 64) {
+    const int b = tid >> 5, c = tid & 31, o = b * 32;
+    for (int i = 0; i < 32; ++i) {
+      double x = 0.0;
+      if (i == c) {
+        x = 1.0 / S[sw_off(o + i, o + i)];
+      } else if (i > c) {
+        double s = 0.0;
+        for (int k = c; k < i; ++k) s -= S[sw_off(o + i, o + k)] * X[sw_off(o + k, o + c)];
+        x = s / S[sw_off(o + i, o + i)];
       }
-      X[sw_off(i, c)] = x;
+      X[sw_off(o + i, o + c)] = x;
     }
+  }
+  // upper-right block is zero
+  for (int e = tid; e < 1024; e += NT) X[sw_off(e >> 5, 32 + (e & 31))] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < 1024; e += NT) {  // T = L21 X11, X11 lower: k ≥ c
+    const int i = e >> 5, c = e & 31;
+    double s = 0.0;
+    for (int k = c; k < 32; ++k) s += S[sw_off(32 + i, k)] * X[sw_off(k, c)];
+    T[e] = s;
+  }
+  __syncthreads();
+  for (int e = tid; e < 1024; e += NT) {  // X21 = −X22 T, X22 lower: k ≤ i
+    const int i = e >> 5, c = e & 31;
+    double s = 0.0;
+    for (int k = 0; k <= i; ++k) s += X[sw_off(32 + i, 32 + k)] * T[k * 32 + c];
+    X[sw_off(32 + i, c)] = -s;
   }
 }
 
@@ -247,7 +306,7 @@ __device__ void write_point_failure(const CholArgs& A, int k, int code) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
+__global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   extern __shared__ __align__(1024) double sm[];
   double* staging = sm;  // aliases the stage ring (used only between k-loops)
   double* Linv = sm + OFF_LINV;
@@ -264,9 +323,10 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
   const SlotGeom g = A.g;
   const int nt = g.nt, M = A.M, p = A.p, r = g.r;
   double* ws = A.ws + (size_t)blockIdx.x * g.slot_d;
-  const PointConst P = A.pc[k];
+  const int mode = A.pc[k].mode;
+  const double nugget = A.pc[k].nugget;
 
-  if (P.mode == MODE_BAD) {
+  if (mode == MODE_BAD) {
     write_point_failure(A, k, LIK_PT_BAD_PARAM);
     return;
   }
@@ -277,8 +337,8 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
   }
   __syncthreads();
 
-  Pipe pp{sm, mbar, 0u};
-  const double tol = g.n * DBL_EPSILON * (1.0 + P.nugget);
+  Pipe pp{sm, mbar, 0u, policy_evict_first(), policy_evict_last()};
+  const double tol = g.n * DBL_EPSILON * (1.0 + nugget);
   double logdet = 0.0;  // meaningful in thread 0
   auto valid_rows = [&](int ti) { return ti == nt ? g.Ra : (ti == nt - 1 ? g.vlast : TB); };
   auto copy_rows = [&](int ti) { return ti == nt ? g.Ra : TB; };
@@ -294,32 +354,14 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
       const int ib = (rb + 1 < nrow) ? j + rb + 1 : -1;
       const int vmine = mine_b ? (ib >= 0 ? valid_rows(ib) : 0) : valid_rows(ia);
       const int mlim = max(0, min(4, (vmine - rbase + 7) >> 3));
-      // C = A_ij − Σ_k L_ik L_jkᵀ, accumulated as acc = −A_ij + Σ L Lᵀ, negated below
-      if (mlim > 0) {
-        frag_load(acc, tile_ptr(mine_b ? ib : ia, j), rbase, cbase, mlim, lane);
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) {
-            acc[mi][ni][0] = -acc[mi][ni][0];
-            acc[mi][ni][1] = -acc[mi][ni][1];
-          }
-      } else {
-        frag_zero(acc);
-      }
+      // acc = −A_ij + Σ_k L_ik L_jkᵀ  (stored negated: C = A_ij − Σ_k L_ik L_jkᵀ)
+      frag_load_neg(acc, tile_ptr(mine_b ? (ib >= 0 ? ib : ia) : ia, j), rbase, cbase, mlim, lane);
       if (j > 0)
         kloop(acc, pp, tile_ptr(ia, 0), copy_rows(ia), ib >= 0 ? tile_ptr(ib, 0) : nullptr,
-              ib >= 0 ? copy_rows(ib) : 0, tile_ptr(j, 0), TB, 2 * j, mine_b, rbase, mlim, cbase,
-              lane);
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          acc[mi][ni][0] = -acc[mi][ni][0];
-          acc[mi][ni][1] = -acc[mi][ni][1];
-        }
+              ib >= 0 ? copy_rows(ib) : 0, tile_ptr(j, 0), TB, CHUNKS * j, mine_b, rbase, mlim,
+              cbase, lane);
       __syncthreads();
-      frag_store(acc, staging + (mine_b ? TILE_D : 0), rbase, cbase, mlim, lane);
+      frag_store<true>(acc, staging + (mine_b ? TILE_D : 0), rbase, cbase, mlim, lane);
       __syncthreads();
       if (rb == 0) {
         // diagonal tile: factor, log-determinant, inverse for this column's solves
@@ -332,26 +374,25 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
           for (int c = 0; c < valid_rows(j); ++c) s += dlog[c];
           logdet += s;
         }
-        trinv64(staging, valid_rows(j), Linv);
+        trinv64(staging, Linv, sm + OFF_SCRATCH);
         __syncthreads();
         if (ib >= 0 && mine_b) {
           frag_zero(acc);
-          if (mlim > 0) {
-            mma_chunk(acc, staging + TILE_D, rbase, mlim, Linv, cbase, lane);
-            mma_chunk(acc, staging + TILE_D + CHUNK_D, rbase, mlim, Linv + CHUNK_D, cbase, lane);
-          }
-          frag_store(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
+#pragma unroll
+          for (int h = 0; h < CHUNKS; ++h)
+            mma_chunk_any(acc, staging + TILE_D + h * CHUNK_D, rbase, mlim, Linv + h * CHUNK_D,
+                          cbase, lane);
+          frag_store<false>(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
         }
       } else {
         // L_ij = C L_jj⁻ᵀ for both tile rows of the block
         frag_zero(acc);
         const double* Sb = staging + (mine_b ? TILE_D : 0);
-        if (mlim > 0) {
-          mma_chunk(acc, Sb, rbase, mlim, Linv, cbase, lane);
-          mma_chunk(acc, Sb + CHUNK_D, rbase, mlim, Linv + CHUNK_D, cbase, lane);
-        }
+#pragma unroll
+        for (int h = 0; h < CHUNKS; ++h)
+          mma_chunk_any(acc, Sb + h * CHUNK_D, rbase, mlim, Linv + h * CHUNK_D, cbase, lane);
         const int ti = mine_b ? ib : ia;
-        if (ti >= 0) frag_store(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
+        if (ti >= 0) frag_store<false>(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
       }
       fence_proxy_async();
       __syncthreads();
@@ -362,14 +403,14 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
   {
     const int mlim = mine_b ? 0 : max(0, min(4, (g.Ra - rbase + 7) >> 3));
     frag_zero(acc);
-    kloop(acc, pp, tile_ptr(nt, 0), g.Ra, nullptr, 0, tile_ptr(nt, 0), g.Ra, 2 * nt, false,
+    kloop(acc, pp, tile_ptr(nt, 0), g.Ra, nullptr, 0, tile_ptr(nt, 0), g.Ra, CHUNKS * nt, false,
           rbase, mlim, cbase, lane);
     __syncthreads();
-    frag_store(acc, staging, rbase, cbase, mlim, lane);
+    frag_store<false>(acc, staging, rbase, cbase, mlim, lane);
     __syncthreads();
   }
   // Steps 5-8 and Eq. (profile)
-  double* Cm = Linv;          // r×r, plain row-major with stride 64
+  double* Cm = Linv;             // r×r, plain row-major with stride 64
   double* Q = staging + TILE_D;  // p×p Cholesky factor of XᵀV⁻¹X (stride 64)
   for (int e = tid; e < r * r; e += NT) {
     const int a = e / r, b = e % r;
@@ -451,6 +492,7 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs A) {
 }  // namespace
 
 size_t chol_smem_bytes() { return (size_t)SMEM_D * sizeof(double); }
+int chol_ctas_per_sm() { return 2; }
 
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st) {
   const size_t smem = chol_smem_bytes();

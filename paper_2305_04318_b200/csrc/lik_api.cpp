@@ -144,7 +144,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
                double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st) {
   const SlotGeom g = lik::make_geom(n, M + p);
   const size_t slot_bytes = g.slot_d * sizeof(double);
-  int W = c->wave_points > 0 ? c->wave_points : c->nsm;
+  int W = c->wave_points > 0 ? c->wave_points : c->nsm * lik::chol_ctas_per_sm();
   W = std::min(W, K);
   {
     size_t fr = 0, tot = 0;

@@ -18,20 +18,21 @@ namespace lik {
 // the augmented row, and −BᵀV⁻¹B as the Schur complement of the last block
 // (§3.3 Steps 2-4).
 //
-// Inside a tile the 64 columns are split into two 64×32 "chunks" (16 KB,
+// Inside a tile the 64 columns are split into four 64×16 "chunks" (8 KB,
 // contiguous), each row-major with an XOR swizzle of the column index so that
 // the DMMA fragment loads from shared memory are bank-conflict free after a
 // 1-D bulk copy (cp.async.bulk) of the chunk.  Because the tiles of one tile
 // row are contiguous, the row panel L[i, 0:j] is one contiguous run of
-// 2j chunks.
+// 4j chunks.
 // ---------------------------------------------------------------------------
 constexpr int TB = 64;              // tile edge
-constexpr int KC = 32;              // chunk width (k-extent of one pipeline stage)
+constexpr int KC = 16;              // chunk width (k-extent of one pipeline stage)
+constexpr int CHUNKS = TB / KC;     // chunks per tile
 constexpr int TILE_D = TB * TB;     // doubles per tile
 constexpr int CHUNK_D = TB * KC;    // doubles per chunk
 
 __host__ __device__ __forceinline__ int sw_off(int row, int col) {
-  return ((col >> 5) << 11) + (row << 5) + ((col & 31) ^ ((row & 3) << 2));
+  return ((col >> 4) << 10) + (row << 4) + ((col & 15) ^ ((row & 3) << 2));
 }
 __host__ __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
@@ -111,5 +112,6 @@ struct CholArgs {
 };
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
 size_t chol_smem_bytes();
+int chol_ctas_per_sm();
 
 }  // namespace lik
