@@ -37,7 +37,7 @@ constexpr int OFF_LINV = NSTAGE * STAGE_D;
 constexpr int OFF_DLOG = OFF_LINV + TILE_D;
 constexpr int OFF_MISC = OFF_DLOG + 64;          // 8 doubles of scalars
 constexpr int OFF_MBAR = OFF_MISC + 8;           // NSTAGE uint64
-constexpr int SMEM_D = OFF_MBAR + NSTAGE + 4;    // + int flags
+constexpr int SMEM_D = OFF_MBAR + NSTAGE + 4;    // + int flags[4], cnt[NSTAGE]
 static_assert(OFF_SCRATCH + 32 * 32 <= OFF_LINV, "staging + scratch must fit in the stage ring");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -177,14 +177,19 @@ __device__ __forceinline__ void frag_zero(Acc& acc) {
 
 struct Pipe {
   double* stages;
-  uint64_t* mbar;
-  uint32_t seq;  // chunks consumed so far (same value in every thread)
+  uint64_t* mbar;     // "full" barriers: complete when a stage's bulk copies landed
+  int* cnt;           // per-stage count of warps done reading it
+  uint32_t seq;       // chunks consumed so far (same value in every thread)
   uint64_t pol_stream, pol_keep;
 };
 
 // acc += Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
 //   A rows of tile a: gA0 + q·CHUNK_D (cA0 rows copied), tile b: gA1 (cA1 rows),
 //   B rows: gB (cB rows).
+// There is no CTA-wide barrier per chunk: each warp waits only for its data
+// (mbarrier), and the last of the 8 warps to finish reading a stage (counted
+// with a shared-memory atomic) refills it with the chunk NSTAGE ahead.  The
+// caller must __syncthreads() between two k-loops.
 __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int cA0,
                                       const double* gA1, int cA1, const double* gB, int cB,
                                       int nq, bool mine_b, int rbase, int mlim, int cbase,
@@ -201,56 +206,103 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int
       bulk_g2s(saddr(st + CHUNK_D), gA1 + (size_t)q * CHUNK_D, cA1 * KC * 8, bar, pp.pol_stream);
     bulk_g2s(saddr(st + 2 * CHUNK_D), gB + (size_t)q * CHUNK_D, cB * KC * 8, bar, pp.pol_keep);
   };
-  if (tid == 0) {
-    issue(0);
-    if (nq > 1) issue(1);
-  }
+  if (tid == 0)
+    for (int q = 0; q < NSTAGE && q < nq; ++q) issue(q);
   for (int q = 0; q < nq; ++q) {
-    if (tid == 0 && q + 2 < nq) issue(q + 2);
     const uint32_t s = (seq + q) % NSTAGE;
     mbar_wait(saddr(&pp.mbar[s]), ((seq + q) / NSTAGE) & 1);
     const double* st = pp.stages + s * STAGE_D;
     mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, cbase, lane);
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();  // this warp's reads of stage s precede the arrival
+      if (atomicAdd(&pp.cnt[s], 1) == NT / 32 - 1) {
+        pp.cnt[s] = 0;
+        if (q + NSTAGE < nq) issue(q + NSTAGE);
+      }
+    }
   }
   pp.seq = seq + nq;
 }
 
-// Unblocked Cholesky of the leading v×v block of a 64×64 tile in shared memory
-// (lower part used).  dlog[c] = log(pivot_c) = 2 log L_cc.  Returns nonzero
-// (uniformly) if a pivot is ≤ tol (R11).  Afterwards rows/columns ≥ v are set
-// to the identity (the padding of V), so the tile is a complete 64×64 factor.
-__device__ int potrf64(double* S, int v, double tol, double* dlog, double* scal, int* flag) {
-  const int tid = threadIdx.x;
-  for (int c = 0; c < v; ++c) {
-    if (tid == 0) {
-      const double d = S[sw_off(c, c)];
-      if (!(d > tol)) {
-        flag[0] = 1;
-      } else {
-        const double l = sqrt(d);
-        dlog[c] = log(d);
-        S[sw_off(c, c)] = l;
-        scal[0] = 1.0 / l;
-      }
-    }
-    __syncthreads();
-    if (flag[0]) return 1;
-    const double inv = scal[0];
-    for (int r = c + 1 + tid; r < v; r += NT) S[sw_off(r, c)] *= inv;
-    __syncthreads();
-    for (int e = tid; e < TILE_D; e += NT) {
-      const int rr = e >> 6, kk = e & 63;
-      if (kk > c && kk <= rr && rr < v) S[sw_off(rr, kk)] -= S[sw_off(rr, c)] * S[sw_off(kk, c)];
-    }
-    __syncthreads();
-  }
-  if (v < TB) {
+// Blocked Cholesky of a 64×64 tile in shared memory (lower part used) whose
+// rows/columns ≥ v are the identity padding of V.  Four 16-column panels:
+//   (a) warp 0 factors the 16×16 diagonal block in registers (shuffles),
+//   (b) the rows below solve against it (one thread per row),
+//   (c) the trailing lower triangle is updated with the panel (all threads).
+// dlog[c] = log(pivot_c) = 2 log L_cc.  Returns nonzero (uniformly) if a pivot
+// is ≤ tol (R11).
+__device__ int potrf64(double* S, int v, double tol, double* dlog, int* flag) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (v < TB) {  // identity padding (those rows of the staging tile were not computed)
     for (int e = tid; e < TILE_D; e += NT) {
       const int rr = e >> 6, kk = e & 63;
       if (rr >= v && kk <= rr) S[sw_off(rr, kk)] = (rr == kk) ? 1.0 : 0.0;
     }
     __syncthreads();
+  }
+  for (int c0 = 0; c0 < TB; c0 += 16) {
+    if (warp == 0) {
+      const int l = lane & 15;
+      double a[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) a[k] = (k <= l) ? S[sw_off(c0 + l, c0 + k)] : 0.0;
+      int bad = 0;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const double piv = __shfl_sync(0xffffffffu, a[c], c);
+        bad |= !(piv > tol);
+        const double lcc = sqrt(piv);
+        const double inv = 1.0 / lcc;
+        if (l == c) {
+          a[c] = lcc;
+          if (lane < 16) dlog[c0 + c] = log(piv);
+        } else if (l > c) {
+          a[c] *= inv;
+        }
+#pragma unroll
+        for (int k = c + 1; k < 16; ++k) {
+          const double lk = __shfl_sync(0xffffffffu, a[c], k);
+          if (l >= k) a[k] -= a[c] * lk;
+        }
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k <= l) S[sw_off(c0 + l, c0 + k)] = a[k];
+      }
+      if (lane == 0 && bad) flag[0] = 1;
+    }
+    __syncthreads();
+    if (flag[0]) return 1;
+    if (c0 + 16 < TB) {
+      // (b) rows below: L[i, c0:c0+16] = S[i, c0:c0+16] L_pp⁻ᵀ
+      for (int i = c0 + 16 + tid; i < TB; i += NT) {
+        double x[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          double s = S[sw_off(i, c0 + c)];
+#pragma unroll
+          for (int k = 0; k < c; ++k) s -= x[k] * S[sw_off(c0 + c, c0 + k)];
+          x[c] = s / S[sw_off(c0 + c, c0 + c)];
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) S[sw_off(i, c0 + c)] = x[c];
+      }
+      __syncthreads();
+      // (c) trailing update of the lower triangle below/right of the panel
+      const int base = c0 + 16, m = TB - base;
+      for (int e = tid; e < m * m; e += NT) {
+        const int i = base + e / m, kk = base + e % m;
+        if (kk <= i) {
+          double s = S[sw_off(i, kk)];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) s -= S[sw_off(i, c0 + c)] * S[sw_off(kk, c0 + c)];
+          S[sw_off(i, kk)] = s;
+        }
+      }
+      __syncthreads();
+    }
   }
   return 0;
 }
@@ -314,6 +366,7 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   double* scal = sm + OFF_MISC;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + OFF_MBAR);
   int* flag = reinterpret_cast<int*>(sm + OFF_MBAR + NSTAGE);
+  int* cnt = flag + 4;
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w >> 1, wc = w & 1;
@@ -333,11 +386,12 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) mbar_init(saddr(&mbar[s]), 1);
     flag[0] = flag[1] = flag[2] = 0;
+    for (int s = 0; s < NSTAGE; ++s) cnt[s] = 0;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   __syncthreads();
 
-  Pipe pp{sm, mbar, 0u, policy_evict_first(), policy_evict_last()};
+  Pipe pp{sm, mbar, cnt, 0u, policy_evict_first(), policy_evict_last()};
   const double tol = g.n * DBL_EPSILON * (1.0 + nugget);
   double logdet = 0.0;  // meaningful in thread 0
   auto valid_rows = [&](int ti) { return ti == nt ? g.Ra : (ti == nt - 1 ? g.vlast : TB); };
@@ -365,7 +419,7 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
       __syncthreads();
       if (rb == 0) {
         // diagonal tile: factor, log-determinant, inverse for this column's solves
-        if (potrf64(staging, valid_rows(j), tol, dlog, scal, flag)) {
+        if (potrf64(staging, valid_rows(j), tol, dlog, flag)) {
           write_point_failure(A, k, LIK_PT_V_NOT_PD);
           return;
         }
