@@ -181,6 +181,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2305_04318_b200 as lik
+    from paper_2305_04318_b200 import multi
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -201,16 +202,14 @@ def main():
     dc, dy, dX, dp, dl = (torch.tensor(a, device=dev) for a in (coords, y, X, P, lam))
     out = lik.Ctx.alloc_outputs(K, M, p, dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    pack_w = M * (2 + p) + 2
-    gathered = torch.empty((world, K, pack_w), dtype=torch.float64, device=dev) if world > 1 else None
+    pack_w = multi.pack_width(M, p)
+    gathered = torch.empty((world * K, pack_w), dtype=torch.float64, device=dev) if world > 1 else None
 
     def step():
         ctx.eval_batch_device(dc, dy, dX, dp, dl, out=out, stream=st)
-        if world > 1:
+        if world > 1:  # the one exchange step: all-gather of the result tables (NCCL / NVLink)
             with torch.cuda.stream(st):
-                packed = torch.cat([out["loglik"], out["sigma2hat"], out["betahat"].reshape(K, -1),
-                                    out["logdetV"][:, None], out["status"][:, None].double()], 1)
-                dist.all_gather_into_tensor(gathered.view(world * K, pack_w), packed)
+                dist.all_gather_into_tensor(gathered, multi.pack(out, M, p, K))
 
     for _ in range(args.warmup):
         with torch.cuda.stream(st):
