@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblik.so")
+LIB_PATH = os.environ.get("LIK_LIBRARY") or os.path.join(HERE, "liblik.so")  # LIK_LIBRARY: debug builds
 
 LIK_OK, LIK_EINVAL, LIK_EDOMAIN, LIK_ERANK, LIK_ENOMEM, LIK_ECUDA, LIK_ENOTIMPL = 0, -1, -2, -3, -4, -5, -6
 PT_OK, PT_V_NOT_PD, PT_XVX_NOT_PD, PT_NEG_RESID, PT_BAD_PARAM = 0, 1, 2, 3, 4

@@ -26,6 +26,17 @@
 #include "../../include/lik.h"
 #include "lik_internal.cuh"
 
+#ifdef LIK_PHASE_TIMERS
+__device__ unsigned long long g_lik_phase[16];
+#define PH_INIT() long long ph_t = clock64(); long long ph_acc[16] = {0}
+#define PH(i) do { const long long t_ = clock64(); ph_acc[i] += t_ - ph_t; ph_t = t_; } while (0)
+#define PH_FLUSH() do { if (threadIdx.x == 0) for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_lik_phase[i_], (unsigned long long)ph_acc[i_]); } while (0)
+#else
+#define PH_INIT() do {} while (0)
+#define PH(i) do {} while (0)
+#define PH_FLUSH() do {} while (0)
+#endif
+
 namespace lik {
 namespace {
 
@@ -225,15 +236,28 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int
   pp.seq = seq + nq;
 }
 
-// Blocked Cholesky of a 64×64 tile in shared memory (lower part used) whose
-// rows/columns ≥ v are the identity padding of V.  Four 16-column panels:
-//   (a) warp 0 factors the 16×16 diagonal block in registers (shuffles),
-//   (b) the rows below solve against it (one thread per row),
-//   (c) the trailing lower triangle is updated with the panel (all threads).
-// dlog[c] = log(pivot_c) = 2 log L_cc.  Returns nonzero (uniformly) if a pivot
-// is ≤ tol (R11).
-__device__ int potrf64(double* S, int v, double tol, double* dlog, int* flag) {
+// Blocked Cholesky + inverse of a 64×64 tile in shared memory (lower part used)
+// whose rows/columns ≥ v are the identity padding of V.  Four 16-column panels:
+//   (a) warp 0 factors the 16×16 diagonal block D_p in registers (shuffles) and
+//       inverts it into X (the diagonal blocks of L⁻¹),
+//   (b) the rows below: L[i, panel] = S[i, panel] · D_p⁻ᵀ (parallel products),
+//   (c) trailing update of the lower triangle with the panel (parallel).
+// Then L⁻¹ is assembled from the D_p⁻¹ by block recursion (16 → 32 → 64):
+//   X_ba = −X_bb (L_ba X_aa)  for the off-diagonal blocks.
+// Every step is a short product with ≤ 32-long dot products, so the phase has no
+// long dependent chains.  dlog[c] = log(pivot_c).  Returns nonzero (uniformly)
+// if a pivot is ≤ tol (R11).  T is a 32×32 scratch.
+#ifdef LIK_PHASE_TIMERS
+#define SUB(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_lik_phase[i], (unsigned long long)(t_ - sub_t)); sub_t = t_; } } while (0)
+#else
+#define SUB(i) do {} while (0)
+#endif
+__device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag, double* X,
+                           double* T) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef LIK_PHASE_TIMERS
+  long long sub_t = clock64();
+#endif
   if (v < TB) {  // identity padding (those rows of the staging tile were not computed)
     for (int e = tid; e < TILE_D; e += NT) {
       const int rr = e >> 6, kk = e & 63;
@@ -243,55 +267,88 @@ __device__ int potrf64(double* S, int v, double tol, double* dlog, int* flag) {
   }
   for (int c0 = 0; c0 < TB; c0 += 16) {
     if (warp == 0) {
+      // Only the pivot chain is serial: one rsqrt per pivot gives L_cc and 1/L_cc;
+      // logs and the inverse use no divisions (the FP64 pipe is shared with the
+      // co-resident CTA's DMMAs, so every dependent FP64 op on this chain is slow).
       const int l = lane & 15;
       double a[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) a[k] = (k <= l) ? S[sw_off(c0 + l, c0 + k)] : 0.0;
       int bad = 0;
+      double my_piv = 1.0, my_rinv = 1.0;
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const double piv = __shfl_sync(0xffffffffu, a[c], c);
         bad |= !(piv > tol);
-        const double lcc = sqrt(piv);
-        const double inv = 1.0 / lcc;
+        const double rinv = rsqrt(piv);
         if (l == c) {
-          a[c] = lcc;
-          if (lane < 16) dlog[c0 + c] = log(piv);
+          a[c] = piv * rinv;
+          my_piv = piv;
+          my_rinv = rinv;
         } else if (l > c) {
-          a[c] *= inv;
+          a[c] *= rinv;
         }
 #pragma unroll
-        for (int k = c + 1; k < 16; ++k) {
-          const double lk = __shfl_sync(0xffffffffu, a[c], k);
-          if (l >= k) a[k] -= a[c] * lk;
+        for (int k = 0; k < 16; ++k) {  // constant trip count: fully unrolled, a[] stays in registers
+          if (k > c) {
+            const double lk = __shfl_sync(0xffffffffu, a[c], k);
+            if (l >= k) a[k] -= a[c] * lk;
+          }
         }
+      }
+      if (lane < 16) dlog[c0 + l] = log(my_piv);
+      // lane l computes column l of D_p⁻¹, right-looking: x = e_l; for each i,
+      // x_i *= 1/D_ii, then x_k −= D_ki x_i for k > i (independent updates, so the
+      // dependent chain is two ops per step).  D_ki is fetched from lane k.
+      double x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = (i == l) ? 1.0 : 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        x[i] *= __shfl_sync(0xffffffffu, my_rinv, i);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k > i) x[k] -= __shfl_sync(0xffffffffu, a[i], k) * x[i];
       }
       if (lane < 16) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
+        for (int k = 0; k < 16; ++k) {
           if (k <= l) S[sw_off(c0 + l, c0 + k)] = a[k];
+          X[sw_off(c0 + k, c0 + l)] = x[k];  // column l of D_p⁻¹
+        }
       }
       if (lane == 0 && bad) flag[0] = 1;
     }
+    SUB(10);
     __syncthreads();
+    SUB(11);
     if (flag[0]) return 1;
     if (c0 + 16 < TB) {
-      // (b) rows below: L[i, c0:c0+16] = S[i, c0:c0+16] L_pp⁻ᵀ
-      for (int i = c0 + 16 + tid; i < TB; i += NT) {
-        double x[16];
+      // (b) L[i, c0+c] = Σ_{k ≤ c} S[i, c0+k] · D_p⁻¹[c][k]  (rows below the panel)
+      const int base = c0 + 16, m = TB - base;
+      double xv[3];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          double s = S[sw_off(i, c0 + c)];
+      for (int q = 0; q < 3; ++q) {
+        const int e = tid + q * NT;
+        xv[q] = 0.0;
+        if (e < m * 16) {
+          const int i = base + (e >> 4), c = e & 15;
+          double s = 0.0;
 #pragma unroll
-          for (int k = 0; k < c; ++k) s -= x[k] * S[sw_off(c0 + c, c0 + k)];
-          x[c] = s / S[sw_off(c0 + c, c0 + c)];
+          for (int k = 0; k < 16; ++k)
+            if (k <= c) s += S[sw_off(i, c0 + k)] * X[sw_off(c0 + c, c0 + k)];
+          xv[q] = s;
         }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) S[sw_off(i, c0 + c)] = x[c];
       }
       __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int e = tid + q * NT;
+        if (e < m * 16) S[sw_off(base + (e >> 4), c0 + (e & 15))] = xv[q];
+      }
+      __syncthreads();
+      SUB(12);
       // (c) trailing update of the lower triangle below/right of the panel
-      const int base = c0 + 16, m = TB - base;
       for (int e = tid; e < m * m; e += NT) {
         const int i = base + e / m, kk = base + e % m;
         if (kk <= i) {
@@ -302,46 +359,49 @@ __device__ int potrf64(double* S, int v, double tol, double* dlog, int* flag) {
         }
       }
       __syncthreads();
+      SUB(13);
     }
   }
-  return 0;
-}
-
-// X = L⁻¹ (64×64 lower triangular) in two levels of 32×32 blocks:
-//   X11 = L11⁻¹, X22 = L22⁻¹ (column-parallel forward substitution, 64 threads),
-//   X21 = −X22 (L21 X11)  (all threads; T = L21 X11 in the 32×32 scratch).
-__device__ void trinv64(const double* S, double* X, double* T) {
-  const int tid = threadIdx.x;
-  if (tid < 64) {
-    const int b = tid >> 5, c = tid & 31, o = b * 32;
-    for (int i = 0; i < 32; ++i) {
-      double x = 0.0;
-      if (i == c) {
-        x = 1.0 / S[sw_off(o + i, o + i)];
-      } else if (i > c) {
-        double s = 0.0;
-        for (int k = c; k < i; ++k) s -= S[sw_off(o + i, o + k)] * X[sw_off(o + k, o + c)];
-        x = s / S[sw_off(o + i, o + i)];
-      }
-      X[sw_off(o + i, o + c)] = x;
-    }
+  // strictly-upper parts of X are zero
+  for (int e = tid; e < TILE_D; e += NT) {
+    const int i = e >> 6, c = e & 63;
+    if ((c >> 4) > (i >> 4)) X[sw_off(i, c)] = 0.0;
   }
-  // upper-right block is zero
-  for (int e = tid; e < 1024; e += NT) X[sw_off(e >> 5, 32 + (e & 31))] = 0.0;
+  // L⁻¹ off-diagonal blocks, level 16 → 32: blocks (1,0) of each 32-block
+  for (int e = tid; e < 2 * 256; e += NT) {  // T_h = L_{(2h+1),(2h)} X_{(2h),(2h)}
+    const int h = e >> 8, i = (e >> 4) & 15, c = e & 15, o = 32 * h;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k >= c) s += S[sw_off(o + 16 + i, o + k)] * X[sw_off(o + k, o + c)];
+    T[e] = s;
+  }
   __syncthreads();
-  for (int e = tid; e < 1024; e += NT) {  // T = L21 X11, X11 lower: k ≥ c
+  for (int e = tid; e < 2 * 256; e += NT) {  // X_{(2h+1),(2h)} = −X_{(2h+1),(2h+1)} T_h
+    const int h = e >> 8, i = (e >> 4) & 15, c = e & 15, o = 32 * h;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k <= i) s += X[sw_off(o + 16 + i, o + 16 + k)] * T[h * 256 + k * 16 + c];
+    X[sw_off(o + 16 + i, o + c)] = -s;
+  }
+  __syncthreads();
+  // level 32 → 64: X21 = −X22 (L21 X11)
+  for (int e = tid; e < 1024; e += NT) {
     const int i = e >> 5, c = e & 31;
     double s = 0.0;
     for (int k = c; k < 32; ++k) s += S[sw_off(32 + i, k)] * X[sw_off(k, c)];
     T[e] = s;
   }
   __syncthreads();
-  for (int e = tid; e < 1024; e += NT) {  // X21 = −X22 T, X22 lower: k ≤ i
+  for (int e = tid; e < 1024; e += NT) {
     const int i = e >> 5, c = e & 31;
     double s = 0.0;
     for (int k = 0; k <= i; ++k) s += X[sw_off(32 + i, 32 + k)] * T[k * 32 + c];
     X[sw_off(32 + i, c)] = -s;
   }
+  SUB(14);
+  return 0;
 }
 
 __device__ void write_point_failure(const CholArgs& A, int k, int code) {
@@ -401,6 +461,7 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   };
 
   Acc acc;
+  PH_INIT();
   for (int j = 0; j < nt; ++j) {
     const int nrow = nt - j + 1;  // tile rows j..nt-1 and the augmented row
     for (int rb = 0; rb < nrow; rb += 2) {
@@ -410,16 +471,20 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
       const int mlim = max(0, min(4, (vmine - rbase + 7) >> 3));
       // acc = −A_ij + Σ_k L_ik L_jkᵀ  (stored negated: C = A_ij − Σ_k L_ik L_jkᵀ)
       frag_load_neg(acc, tile_ptr(mine_b ? (ib >= 0 ? ib : ia) : ia, j), rbase, cbase, mlim, lane);
+      PH(0);
       if (j > 0)
         kloop(acc, pp, tile_ptr(ia, 0), copy_rows(ia), ib >= 0 ? tile_ptr(ib, 0) : nullptr,
               ib >= 0 ? copy_rows(ib) : 0, tile_ptr(j, 0), TB, CHUNKS * j, mine_b, rbase, mlim,
               cbase, lane);
+      PH(1);
       __syncthreads();
+      PH(2);
       frag_store<true>(acc, staging + (mine_b ? TILE_D : 0), rbase, cbase, mlim, lane);
       __syncthreads();
+      PH(3);
       if (rb == 0) {
         // diagonal tile: factor, log-determinant, inverse for this column's solves
-        if (potrf64(staging, valid_rows(j), tol, dlog, flag)) {
+        if (potrf_inv64(staging, valid_rows(j), tol, dlog, flag, Linv, sm + OFF_SCRATCH)) {
           write_point_failure(A, k, LIK_PT_V_NOT_PD);
           return;
         }
@@ -428,8 +493,9 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
           for (int c = 0; c < valid_rows(j); ++c) s += dlog[c];
           logdet += s;
         }
-        trinv64(staging, Linv, sm + OFF_SCRATCH);
+        PH(4);
         __syncthreads();
+        PH(5);
         if (ib >= 0 && mine_b) {
           frag_zero(acc);
 #pragma unroll
@@ -448,8 +514,10 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
         const int ti = mine_b ? ib : ia;
         if (ti >= 0) frag_store<false>(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
       }
+      PH(6);
       fence_proxy_async();
       __syncthreads();
+      PH(7);
     }
   }
 
@@ -541,11 +609,25 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
     A.logdetV[k] = ldV;
     A.status[k] = flag[2] ? LIK_PT_NEG_RESID : LIK_PT_OK;
   }
+  PH(8);
+  PH_FLUSH();
 }
 
 }  // namespace
 
 size_t chol_smem_bytes() { return (size_t)SMEM_D * sizeof(double); }
+
+#ifdef LIK_PHASE_TIMERS
+extern "C" int lik_debug_phase_cycles(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, g_lik_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_lik_phase, z, sizeof z);
+  }
+  return 0;
+}
+#endif
 int chol_ctas_per_sm() { return 2; }
 
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st) {
