@@ -76,7 +76,8 @@ struct PointConst {
 
 // Per-point Chebyshev table of ln ρ(z) on binary octaves z ∈ [2^e, 2^{e+1}),
 // e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1.  Each octave stores CHEB_STRIDE
-// doubles: a base H_o followed by CHEB_N Chebyshev coefficients of
+// doubles: a base H_o followed by the CHEB_N monomial coefficients (in
+// t = z/2^e·2 − 3 ∈ [−1, 1)) of the degree-19 Chebyshev interpolant of
 // h(z) = ln ρ(z) + z − H_o, so that ln ρ = (H_o + h(z)) − z.  Below 2^CHEB_ELO
 // the exact evaluation is used; at and above 2^e_zero ρ = 0.
 constexpr int CHEB_N = 20;

@@ -139,21 +139,43 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
     f[idx] = v;
   }
   __syncthreads();
-  // per octave: base H_o = g at the middle node, coefficients of g − H_o (DCT-II)
-  double* T = table + (size_t)blockIdx.x * TABLE_D;
-  for (int idx = tid; idx < CHEB_NOCT * CHEB_STRIDE; idx += 256) {
-    const int o = idx / CHEB_STRIDE, j = idx % CHEB_STRIDE - 1;
-    double c = 0.0;
+  // per octave: base H_o = g at the middle node; Chebyshev coefficients of g − H_o
+  // (DCT-II), then converted to monomial coefficients in t (T_j has integer
+  // coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
+  __shared__ double cheb[CHEB_NOCT * CHEB_N];
+  __shared__ double tco[CHEB_N * CHEB_N];  // tco[j][k] = coefficient of t^k in T_j
+  if (tid == 0) {
+    for (int e = 0; e < CHEB_N * CHEB_N; ++e) tco[e] = 0.0;
+    tco[0] = 1.0;
+    tco[CHEB_N + 1] = 1.0;
+    for (int jj = 2; jj < CHEB_N; ++jj)
+      for (int kk = 0; kk < CHEB_N; ++kk)
+        tco[jj * CHEB_N + kk] = (kk > 0 ? 2.0 * tco[(jj - 1) * CHEB_N + kk - 1] : 0.0) -
+                                tco[(jj - 2) * CHEB_N + kk];
+  }
+  for (int idx = tid; idx < CHEB_NOCT * CHEB_N; idx += 256) {
+    const int o = idx / CHEB_N, jj = idx % CHEB_N;
+    double cc = 0.0;
     if (CHEB_ELO + o < ez) {
       const double H = f[o * CHEB_N + CHEB_N / 2];
-      if (j < 0) {
-        c = H;
+      for (int ii = 0; ii < CHEB_N; ++ii) cc += (f[o * CHEB_N + ii] - H) * cospi(jj * (ii + 0.5) / CHEB_N);
+      cc *= (jj == 0 ? 1.0 : 2.0) / CHEB_N;
+    }
+    cheb[idx] = cc;
+  }
+  __syncthreads();
+  double* T = table + (size_t)blockIdx.x * TABLE_D;
+  for (int idx = tid; idx < CHEB_NOCT * CHEB_STRIDE; idx += 256) {
+    const int o = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 1;
+    double a = 0.0;
+    if (CHEB_ELO + o < ez) {
+      if (kk < 0) {
+        a = f[o * CHEB_N + CHEB_N / 2];  // H_o
       } else {
-        for (int i = 0; i < CHEB_N; ++i) c += (f[o * CHEB_N + i] - H) * cospi(j * (i + 0.5) / CHEB_N);
-        c *= (j == 0 ? 1.0 : 2.0) / CHEB_N;
+        for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[o * CHEB_N + jj] * tco[jj * CHEB_N + kk];
       }
     }
-    T[idx] = c;
+    T[idx] = a;
   }
 }
 
@@ -210,20 +232,51 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
     sy[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj + 1] : 0.0;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < TILE_D; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    const int gi = i * TB + r, gj = j * TB + c;
-    double v;
-    if (gi >= g.n || gj >= g.n) {
-      v = (gi == gj) ? 1.0 : 0.0;
-    } else if (gi == gj) {
-      v = 1.0 + P.nugget;
-    } else if (i == j && c > r) {
-      v = 0.0;
-    } else {
-      v = matern_rho_table(P, coef, sx[0][r] - sx[1][c], sy[0][r] - sy[1][c]);
+  // thread -> column c, rows r0 + 4q (q < 16): the warp covers 32 consecutive
+  // columns of one row, so stores are coalesced and the table reads of a warp
+  // mostly hit the same octave.
+  const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
+  const double xj = sx[1][c], yj = sy[1][c];
+  // all elements of the tile are off-diagonal Matérn values (no padding / diagonal)?
+  const bool regular = (i > j) && ((i + 1) * TB <= g.n);
+  unsigned slow = 0u;
+  if (P.mode == MODE_BESSEL) {
+#pragma unroll 2
+    for (int q = 0; q < 16; q += 2) {
+      const int ra = r0 + 4 * q, rb = ra + 4;
+      double va, vb;
+      matern_rho_table2(P, coef, sx[0][ra] - xj, sy[0][ra] - yj, sx[0][rb] - xj, sy[0][rb] - yj,
+                        va, vb, slow, q);
+      T[sw_off(ra, c)] = va;
+      T[sw_off(rb, c)] = vb;
     }
-    T[sw_off(r, c)] = v;
+  } else {
+#pragma unroll 4
+    for (int q = 0; q < 16; ++q) {
+      const int ra = r0 + 4 * q;
+      T[sw_off(ra, c)] = exp(-2.0 * aniso_d2(P, sx[0][ra] - xj, sy[0][ra] - yj));
+    }
+  }
+  if (!regular || slow) {
+    // fix-up pass (rewrites): padding, diagonal, unused upper triangle, outside the table
+#pragma unroll 1
+    for (int q = 0; q < 16; ++q) {
+      const int r = r0 + 4 * q;
+      const int gi = i * TB + r, gj = j * TB + c;
+      double v;
+      if (gi >= g.n || gj >= g.n) {
+        v = (gi == gj) ? 1.0 : 0.0;
+      } else if (gi == gj) {
+        v = 1.0 + P.nugget;
+      } else if (i == j && c > r) {
+        v = 0.0;
+      } else if ((slow >> q) & 1u) {
+        v = matern_rho_exact(P, sx[0][r] - xj, sy[0][r] - yj);
+      } else {
+        continue;
+      }
+      T[sw_off(r, c)] = v;
+    }
   }
 }
 
