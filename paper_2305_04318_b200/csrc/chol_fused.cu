@@ -97,6 +97,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;\n" ::: "memory");
 }
@@ -141,6 +144,54 @@ __device__ __forceinline__ void mma_chunk_any(Acc& acc, const double* Ab, int rb
     mma_chunk<true>(acc, Ab, rbase, 4, Bb, cbase, lane);
   else if (mlim > 0)
     mma_chunk<false>(acc, Ab, rbase, mlim, Bb, cbase, lane);
+}
+
+// acc = C · L⁻ᵀ for this warp's 32×32 tile (C rows in shared memory, 64 columns in
+// CHUNKS chunks; X = L⁻¹ lower triangular).  (C L⁻ᵀ)[r][c] = Σ_{k ≤ c} C[r][k] X[c][k],
+// so DMMA k-steps entirely above the warp's columns are skipped (compile time, WC =
+// warp column block): half the multiply-adds of the dense product.
+template <int WC, bool MFULL>
+__device__ __forceinline__ void trsm_tri(Acc& acc, const double* __restrict__ Sb, int rbase,
+                                         int mlim, const double* __restrict__ X, int lane) {
+  const int lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
+  constexpr int cb = WC * 32;
+#pragma unroll
+  for (int h = 0; h < CHUNKS; ++h) {
+    if (KC * h > cb + 31) continue;
+    const double* Ab = Sb + h * CHUNK_D;
+    const double* Bb = X + h * CHUNK_D;
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int k0 = KC * h + 4 * kk;
+      if (k0 > cb + 31) continue;
+      const int kcol = ((kk * 4) ^ sw) + lc;
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        if (cb + ni * 8 + 7 >= k0) b[ni] = Bb[(cb + ni * 8 + lr) * KC + kcol];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+        if (MFULL || mi < mlim) {
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+            if (cb + ni * 8 + 7 >= k0) dmma(acc[mi][ni], a[mi], b[ni]);
+        }
+    }
+  }
+}
+
+__device__ __forceinline__ void trsm_any(Acc& acc, const double* Sb, int rbase, int mlim,
+                                         const double* X, int wc, int lane) {
+  if (mlim <= 0) return;
+  if (wc == 0) {
+    if (mlim == 4) trsm_tri<0, true>(acc, Sb, rbase, 4, X, lane);
+    else trsm_tri<0, false>(acc, Sb, rbase, mlim, X, lane);
+  } else {
+    if (mlim == 4) trsm_tri<1, true>(acc, Sb, rbase, 4, X, lane);
+    else trsm_tri<1, false>(acc, Sb, rbase, mlim, X, lane);
+  }
 }
 
 __device__ __forceinline__ void frag_load_neg(Acc& acc, const double* __restrict__ T, int rbase,
@@ -467,6 +518,25 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
     for (int rb = 0; rb < nrow; rb += 2) {
       const int ia = j + rb;
       const int ib = (rb + 1 < nrow) ? j + rb + 1 : -1;
+      if (tid == 0) {
+        // L2 prefetch for the next row block: its A_ij tiles (initial accumulators)
+        // and the first chunks of its A panels, so neither waits on HBM.
+        int nj = j, na = ia + 2;
+        if (na > nt) { nj = j + 1; na = j + 1; }
+        if (nj < nt) {
+          const int nb = (na + 1 <= nt) ? na + 1 : -1;
+          prefetch_l2(tile_ptr(na, nj), (uint32_t)copy_rows(na) * TB * 8);
+          if (nb >= 0) prefetch_l2(tile_ptr(nb, nj), (uint32_t)copy_rows(nb) * TB * 8);
+          if (nj > 0) {
+            const int nq = min(NSTAGE, CHUNKS * nj);
+            for (int q = 0; q < nq; ++q) {
+              prefetch_l2(tile_ptr(na, 0) + (size_t)q * CHUNK_D, (uint32_t)copy_rows(na) * KC * 8);
+              if (nb >= 0)
+                prefetch_l2(tile_ptr(nb, 0) + (size_t)q * CHUNK_D, (uint32_t)copy_rows(nb) * KC * 8);
+            }
+          }
+        }
+      }
       const int vmine = mine_b ? (ib >= 0 ? valid_rows(ib) : 0) : valid_rows(ia);
       const int mlim = max(0, min(4, (vmine - rbase + 7) >> 3));
       // acc = −A_ij + Σ_k L_ik L_jkᵀ  (stored negated: C = A_ij − Σ_k L_ik L_jkᵀ)
@@ -498,19 +568,13 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
         PH(5);
         if (ib >= 0 && mine_b) {
           frag_zero(acc);
-#pragma unroll
-          for (int h = 0; h < CHUNKS; ++h)
-            mma_chunk_any(acc, staging + TILE_D + h * CHUNK_D, rbase, mlim, Linv + h * CHUNK_D,
-                          cbase, lane);
+          trsm_any(acc, staging + TILE_D, rbase, mlim, Linv, wc, lane);
           frag_store<false>(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
         }
       } else {
         // L_ij = C L_jj⁻ᵀ for both tile rows of the block
         frag_zero(acc);
-        const double* Sb = staging + (mine_b ? TILE_D : 0);
-#pragma unroll
-        for (int h = 0; h < CHUNKS; ++h)
-          mma_chunk_any(acc, Sb + h * CHUNK_D, rbase, mlim, Linv + h * CHUNK_D, cbase, lane);
+        trsm_any(acc, staging + (mine_b ? TILE_D : 0), rbase, mlim, Linv, wc, lane);
         const int ti = mine_b ? ib : ia;
         if (ti >= 0) frag_store<false>(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
       }
