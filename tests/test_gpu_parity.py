@@ -130,6 +130,17 @@ def test_parity_C4_bench_launch_sampled(ctx, orc):
     assert np.all(np.isfinite(gpu["loglik"]))
 
 
+def test_parity_C5_sampled(ctx, orc):
+    """C5 (n = 5,000, the large-matrix stress config): full K on the GPU, a sample
+    of points (incl. κ = 100 and κ = ½) recomputed by the oracle."""
+    coords, y, X, P, lam = synthgen.make_inputs("C5")
+    gpu = ctx.eval_batch(coords, y, X, P, lam)
+    sel = np.unique(np.r_[[0, 1], np.nonzero(P[:, 1] > 99)[0][:1], np.nonzero(np.isclose(P[:, 1], 0.5))[0][:1]])
+    ref = _oracle(orc, coords, y, X, P[sel], lam)
+    assert_parity({k: v[sel] for k, v in gpu.items()}, ref, label="C5")
+    assert np.all(gpu["status"] == 0)
+
+
 # --------------------------------------------------------------------------- edge cases
 def test_status_codes(ctx, orc):
     coords, y, X = synthgen.make_dataset("C1")
