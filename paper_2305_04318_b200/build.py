@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 
 if __name__ == "__main__":
     if "--phase-timers" in sys.argv:
-        print(build(force=True, defines=("LIK_PHASE_TIMERS",), out=os.path.join(HERE, "liblik_phase.so")))
+        extra = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
+        print(build(force=True, defines=("LIK_PHASE_TIMERS",) + extra, out=os.path.join(HERE, "liblik_phase.so")))
     else:
         build(force="--force" in sys.argv, verbose="-v" in sys.argv)
         print(LIB)
