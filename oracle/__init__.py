@@ -57,7 +57,7 @@ def lib():
         L.oracle_validate.argtypes = [_I, _I, _PD, _PD, _PD, _I, _PD, _I, _PD]
         L.oracle_eval.restype = _I
         L.oracle_eval.argtypes = [_I, _I, _PD, _PD, _PD, _I, _PD, _I, _PD,
-                                  _PD, _PD, _PD, _PD, _PI, _PD, _PD, _PD, _PD, _I]
+                                  _PD, _PD, _PD, _PD, _PI, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _I]
         _lib = L
     return _lib
 
@@ -120,7 +120,8 @@ def eval_batch(coords, y, X, params, lambdas, nthreads: int | None = None, summa
     """Batched profile log-likelihood, ABI output layout.
 
     Returns dict(rc, loglik K×M, betahat K×M×p, sigma2hat K×M, logdetV K, status K
-    [, ssqYX K×r×r, detReml K, ssqResidual K×M, qdirect K×M]).
+    [, ssqYX K×r×r, detReml K, ssqResidual K×M, qdirect K×M, ssqBetahat K×M,
+       loglik_reml K×M, sigma2_reml K×M]).
     """
     coords, y, X, lambdas = map(_c, (coords, y, X, lambdas))
     params = _c(params).reshape(-1, 5)
@@ -132,7 +133,9 @@ def eval_batch(coords, y, X, params, lambdas, nthreads: int | None = None, summa
                status=np.full(K, -1, dtype=np.int32))
     if summaries:
         out.update(ssqYX=np.full((K, r, r), np.nan), detReml=np.full(K, np.nan),
-                   ssqResidual=np.full((K, M), np.nan), qdirect=np.full((K, M), np.nan))
+                   ssqResidual=np.full((K, M), np.nan), qdirect=np.full((K, M), np.nan),
+                   ssqBetahat=np.full((K, M), np.nan), loglik_reml=np.full((K, M), np.nan),
+                   sigma2_reml=np.full((K, M), np.nan))
     nt = nthreads or (os.cpu_count() or 1)
     nul = ctypes.cast(None, _PD)
     rc = lib().oracle_eval(
@@ -141,6 +144,7 @@ def eval_batch(coords, y, X, params, lambdas, nthreads: int | None = None, summa
         out["status"].ctypes.data_as(_PI),
         _p(out["ssqYX"]) if summaries else nul, _p(out["detReml"]) if summaries else nul,
         _p(out["ssqResidual"]) if summaries else nul, _p(out["qdirect"]) if summaries else nul,
-        int(nt))
+        _p(out["ssqBetahat"]) if summaries else nul, _p(out["loglik_reml"]) if summaries else nul,
+        _p(out["sigma2_reml"]) if summaries else nul, int(nt))
     out["rc"] = rc
     return out

@@ -198,6 +198,7 @@ struct PointResult {
   std::vector<double> ssqYX;    // Table 1 ssqYX, r×r, r = M + p, columns [y'_1..y'_M | X]
   std::vector<double> ssqBetahat, ssqResidual, qdirect;  // M each
   std::vector<double> loglik, sigma2, beta;               // M, M, M×p
+  std::vector<double> loglik_reml, sigma2_reml;           // M, M (Appendix, REML)
 };
 
 // ---------------------------------------------------------------------------
@@ -219,6 +220,8 @@ PointResult eval_point(int n, int p, const double* coords, const double* X, int 
   R.loglik.assign(M, -INFINITY);
   R.sigma2.assign(M, NAN);
   R.beta.assign((size_t)M * p, NAN);
+  R.loglik_reml.assign(M, -INFINITY);
+  R.sigma2_reml.assign(M, NAN);
   if (!params_valid(w)) { R.status = PT_BAD_PARAM; return R; }
 
   // Step 1: Matérn variance matrix V
@@ -284,6 +287,14 @@ PointResult eval_point(int n, int p, const double* coords, const double* X, int 
                        n * std::log(2.0 * kPi) + n;
     R.loglik[m] = -0.5 * m2l;
     R.sigma2[m] = sigma2;
+    // REML (Appendix): σ̂²_reml = q/(n−p) (Eq. sigmahat_reml_y) and Eq. remlpro
+    // (P:902-905): −2ℓ*_p = (n−p) log(q/(n−p)) + log|V| + log|XᵀV⁻¹X|
+    //                      − 2(λ−1)Σ log y + n log 2π + n − p
+    const double s2r = q / (n - p);
+    const double m2lr = (n - p) * std::log(s2r) + logdet + detReml -
+                        2.0 * (lambdas[m] - 1.0) * S + n * std::log(2.0 * kPi) + (n - p);
+    R.loglik_reml[m] = -0.5 * m2lr;
+    R.sigma2_reml[m] = s2r;
     for (int a = 0; a < p; ++a) R.beta[(size_t)m * p + a] = beta[a];
   }
   return R;
@@ -353,12 +364,13 @@ int oracle_validate(int n, int p, const double* coords, const double* y, const d
 // Full batched evaluation with the ABI's output layout:
 //   loglik K×M, betahat K×M×p, sigma2hat K×M, logdetV K, status K.
 // Optional (may be NULL): ssqYX K×r×r, detReml K, ssqResidual K×M (Step 8 form),
-// qdirect K×M (Eq. 4 form).  nthreads ≥ 1 std::threads over points.
+// qdirect K×M (Eq. 4 form), ssqBetahat K×M, loglik_reml K×M (Eq. remlpro),
+// sigma2_reml K×M.  nthreads ≥ 1 std::threads over points.
 int oracle_eval(int n, int p, const double* coords, const double* y, const double* X, int K,
                 const double* params, int M, const double* lambdas, double* loglik,
                 double* betahat, double* sigma2hat, double* logdetV, int* status,
                 double* ssqYX, double* detReml, double* ssqResidual, double* qdirect,
-                int nthreads) {
+                double* ssqBetahat, double* loglik_reml, double* sigma2_reml, int nthreads) {
   int rc = validate(n, p, coords, y, X, K, params, M, lambdas);
   if (rc != OK) return rc;
   if (!loglik || !betahat || !sigma2hat || !logdetV || !status) return EINVAL_;
@@ -383,6 +395,9 @@ int oracle_eval(int n, int p, const double* coords, const double* y, const doubl
         for (int a = 0; a < p; ++a) betahat[((size_t)k * M + m) * p + a] = R.beta[(size_t)m * p + a];
         if (ssqResidual) ssqResidual[(size_t)k * M + m] = R.ssqResidual[m];
         if (qdirect) qdirect[(size_t)k * M + m] = R.qdirect[m];
+        if (ssqBetahat) ssqBetahat[(size_t)k * M + m] = R.ssqBetahat[m];
+        if (loglik_reml) loglik_reml[(size_t)k * M + m] = R.loglik_reml[m];
+        if (sigma2_reml) sigma2_reml[(size_t)k * M + m] = R.sigma2_reml[m];
       }
       if (ssqYX) for (int t = 0; t < r * r; ++t) ssqYX[(size_t)k * r * r + t] = R.ssqYX[t];
       if (detReml) detReml[k] = R.detReml;

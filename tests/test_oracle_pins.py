@@ -452,3 +452,49 @@ def test_thread_determinism(orc):
     b = orc.eval_batch(coords, y, X, P, lam, nthreads=5)
     for k in ("loglik", "betahat", "sigma2hat", "logdetV", "status"):
         assert np.array_equal(a[k], b[k])
+
+
+# --------------------------------------------------------------------------- REML (Appendix)
+def test_spec_n3_reml_example(orc):
+    g = _gold("spec_n3_ols.json")
+    coords = _far_sites(3, np.random.default_rng(0))
+    y = np.array(g["y_prime"]) + 1.0
+    out = orc.eval_batch(coords, y, np.ones((3, 1)), [[1.0, 0.7, 0.0, 1.0, 0.0]], [1.0], summaries=True)
+    assert out["sigma2_reml"][0, 0] == pytest.approx(g["sigma2hat_reml"], rel=1e-15)
+    assert -2 * out["loglik_reml"][0, 0] == pytest.approx(g["minus2_loglik_reml"], rel=1e-15)
+    assert out["detReml"][0] == pytest.approx(math.log(3.0), rel=1e-15)
+
+
+def test_reml_searle_identities(orc):
+    """Appendix: with an explicit full-rank contrast A (AX = 0, orthonormal
+    rows, scipy null space), y* = A y' and the exact REML likelihood of y*,
+      y*ᵀ(AVAᵀ)⁻¹y* = (y'−Xβ̂)ᵀV⁻¹(y'−Xβ̂)                 (Searle, 2nd identity)
+      −2ℓ*_p(paper) − (−2ℓ*_p(y*)) + 2(λ−1)Σ log y = p log 2π + log|XᵀX|
+    (the paper's |AVAᵀ| = |V||XᵀV⁻¹X| holds up to the constant |XᵀX|⁻¹ for orthonormal A).
+    V from the κ = 3/2 closed form (no Bessel), dense linear algebra from numpy."""
+    coords, y, X = synthgen.make_dataset("C1")
+    n, p = X.shape
+    A = sla.null_space(X.T).T  # (n−p) × n, orthonormal rows, A X = 0
+    const = p * math.log(2 * math.pi) + np.linalg.slogdet(X.T @ X)[1]
+    lam = [0.25, 0.9]
+    for w in ([900.0, 1.5, 0.2, 1.0, 0.0], [400.0, 1.5, 0.7, 1.0, 0.0]):
+        out = orc.eval_batch(coords, y, X, [w], lam, summaries=True)
+        D = np.sqrt(((coords[:, None, :] - coords[None, :, :]) ** 2).sum(-1)) / w[0]
+        z = math.sqrt(12) * D
+        V = (1 + z) * np.exp(-z) + w[2] * np.eye(n)
+        AVA = A @ V @ A.T
+        for m, l in enumerate(lam):
+            yp = (y ** l - 1) / l
+            ys = A @ yp
+            qstar = ys @ np.linalg.solve(AVA, ys)
+            assert qstar == pytest.approx(out["qdirect"][0, m], rel=1e-10)
+            s2 = qstar / (n - p)
+            assert out["sigma2_reml"][0, m] == pytest.approx(s2, rel=1e-10)
+            m2l_exact = (n - p) * math.log(s2) + np.linalg.slogdet(AVA)[1] + (n - p) * (1 + math.log(2 * math.pi))
+            jac = -2 * (l - 1) * np.log(y).sum()
+            assert -2 * out["loglik_reml"][0, m] - m2l_exact - jac == pytest.approx(const, abs=1e-9)
+        # detReml = log|XᵀV⁻¹X| (Table 1)
+        assert out["detReml"][0] == pytest.approx(np.linalg.slogdet(X.T @ np.linalg.solve(V, X))[1], rel=1e-11)
+        # ssqYX blocks (Table 1): y'ᵀV⁻¹y' on the diagonal, XᵀV⁻¹X lower-right, XᵀV⁻¹y' lower-left
+        B = np.column_stack([(y ** l - 1) / l for l in lam] + [X])
+        np.testing.assert_allclose(out["ssqYX"][0], B.T @ np.linalg.solve(V, B), rtol=1e-10)
