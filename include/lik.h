@@ -112,6 +112,27 @@ int lik_eval_batch_device(lik_ctx* ctx, int n, int p, const double* coords, cons
                           const double* lambdas, double* loglik, double* betahat,
                           double* sigma2hat, double* logdetV, int* status, void* cuda_stream);
 
+/* lik_eval_batch_device plus the Table-1 summaries and the REML profile
+ * likelihood (Table 1, Appendix).
+ * Extra outputs (device pointers; each may be NULL to skip it):
+ *   detReml     K      log|XᵀV⁻¹X| (Table 1 detReml; Step 5)
+ *   ssqYX       K×r×r  [y'_1..y'_M | X]ᵀ V⁻¹ [y'_1..y'_M | X], r = M + p (Table 1
+ *                      ssqYX: y'ᵀV⁻¹y' upper-left diagonal, XᵀV⁻¹X lower-right,
+ *                      XᵀV⁻¹y' lower-left; Step 4)
+ *   ssqBetahat  K×M    (Xβ̂)ᵀV⁻¹(Xβ̂) (Step 7)
+ *   ssqResidual K×M    ssqYX_yy − ssqBetahat (Step 8; unclamped)
+ *   loglik_reml K×M    ℓ*_p of Eq. remlpro:
+ *                      −2ℓ*_p = (n−p) log(q/(n−p)) + log|V| + log|XᵀV⁻¹X|
+ *                               − 2(λ−1)Σ log y + n log 2π + n − p
+ *   sigma2hat_reml K×M q/(n−p) (Eq. sigmahat_reml_y)
+ * Failed points get NaN summaries and −inf REML likelihoods (same status). */
+int lik_eval_batch_device_ex(lik_ctx* ctx, int n, int p, const double* coords, const double* y,
+                             const double* X, int K, const double* params, int M,
+                             const double* lambdas, double* loglik, double* betahat,
+                             double* sigma2hat, double* logdetV, int* status, double* detReml,
+                             double* ssqYX, double* ssqBetahat, double* ssqResidual,
+                             double* loglik_reml, double* sigma2hat_reml, void* cuda_stream);
+
 /* Accumulated per-stage device time (ms, from CUDA events on the launching
  * stream) and launch counts since the last reset; arrays of LIK_NSTAGES.
  * Requires LIK_FLAG_TIMING (else LIK_EINVAL). */

@@ -27,7 +27,7 @@ FLAG_TIMING = 1
 STAGES = ("prep", "setup", "matern_build", "chol_fused")
 ABI_SYMBOLS = ("lik_create", "lik_destroy", "lik_last_error", "lik_eval_batch",
                "lik_eval_batch_device", "lik_get_stage_times", "lik_reset_stage_times",
-               "lik_set_wave_points", "lik_debug_build_V")
+               "lik_set_wave_points", "lik_debug_build_V", "lik_eval_batch_device_ex")
 
 _lib = None
 _PD = ctypes.POINTER(ctypes.c_double)
@@ -60,6 +60,8 @@ def lib():
         L.lik_eval_batch.restype = i
         L.lik_eval_batch_device.argtypes = sig + [_VP]
         L.lik_eval_batch_device.restype = i
+        L.lik_eval_batch_device_ex.argtypes = sig + [_VP] * 6 + [_VP]
+        L.lik_eval_batch_device_ex.restype = i
         L.lik_get_stage_times.argtypes = [_VP, _PD, ctypes.POINTER(ctypes.c_longlong)]
         L.lik_get_stage_times.restype = i
         L.lik_reset_stage_times.argtypes = [_VP]
@@ -162,6 +164,30 @@ class Ctx:
             self._h, n, p, _tptr(coords), _tptr(y), _tptr(X), K, _tptr(params), M, _tptr(lambdas),
             _tptr(out["loglik"]), _tptr(out["betahat"]), _tptr(out["sigma2hat"]),
             _tptr(out["logdetV"]), _tptr(out["status"]), ctypes.c_void_p(stream.cuda_stream))
+        self._check(rc)
+        return out
+
+    def eval_batch_device_ex(self, coords, y, X, params, lambdas, stream=None):
+        """lik_eval_batch_device_ex: the outputs of eval_batch_device plus the Table-1
+        summaries (detReml, ssqYX, ssqBetahat, ssqResidual) and the REML profile
+        likelihood (loglik_reml, sigma2hat_reml), as torch CUDA tensors."""
+        import torch
+        n, p = X.shape
+        K, M = params.shape[0], lambdas.shape[0]
+        r = M + p
+        out = self.alloc_outputs(K, M, p, X.device)
+        f = dict(dtype=torch.float64, device=X.device)
+        out.update(detReml=torch.empty(K, **f), ssqYX=torch.empty((K, r, r), **f),
+                   ssqBetahat=torch.empty((K, M), **f), ssqResidual=torch.empty((K, M), **f),
+                   loglik_reml=torch.empty((K, M), **f), sigma2hat_reml=torch.empty((K, M), **f))
+        if stream is None:
+            stream = torch.cuda.current_stream(X.device)
+        rc = lib().lik_eval_batch_device_ex(
+            self._h, n, p, _tptr(coords), _tptr(y), _tptr(X), K, _tptr(params), M, _tptr(lambdas),
+            _tptr(out["loglik"]), _tptr(out["betahat"]), _tptr(out["sigma2hat"]),
+            _tptr(out["logdetV"]), _tptr(out["status"]), _tptr(out["detReml"]), _tptr(out["ssqYX"]),
+            _tptr(out["ssqBetahat"]), _tptr(out["ssqResidual"]), _tptr(out["loglik_reml"]),
+            _tptr(out["sigma2hat_reml"]), ctypes.c_void_p(stream.cuda_stream))
         self._check(rc)
         return out
 

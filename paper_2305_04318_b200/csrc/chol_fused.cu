@@ -483,7 +483,16 @@ __device__ void write_point_failure(const CholArgs& A, int k, int code) {
   for (int e = tid; e < A.M; e += NT) {
     A.loglik[(size_t)k * A.M + e] = -INFINITY;
     A.sigma2hat[(size_t)k * A.M + e] = nan;
+    if (A.ssqBetahat) A.ssqBetahat[(size_t)k * A.M + e] = nan;
+    if (A.ssqResidual) A.ssqResidual[(size_t)k * A.M + e] = nan;
+    if (A.loglik_reml) A.loglik_reml[(size_t)k * A.M + e] = -INFINITY;
+    if (A.sigma2hat_reml) A.sigma2hat_reml[(size_t)k * A.M + e] = nan;
   }
+  if (A.ssqYX) {
+    const int r = A.M + A.p;
+    for (int e = tid; e < r * r; e += NT) A.ssqYX[(size_t)k * r * r + e] = nan;
+  }
+  if (A.detReml && tid == 0) A.detReml[k] = nan;
   for (int e = tid; e < A.M * A.p; e += NT) A.betahat[(size_t)k * A.M * A.p + e] = nan;
   if (tid == 0) {
     A.logdetV[k] = nan;
@@ -616,6 +625,8 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
     Cm[a * 64 + b] = staging[sw_off(a, b)];
   }
   __syncthreads();
+  if (A.ssqYX)
+    for (int e = tid; e < r * r; e += NT) A.ssqYX[(size_t)k * r * r + e] = Cm[(e / r) * 64 + e % r];
   if (tid == LEAD_TID) {
     double xmax = 0.0;
     for (int a = 0; a < p; ++a) xmax = fmax(xmax, Cm[(M + a) * 64 + (M + a)]);
@@ -638,6 +649,10 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
     }
     flag[1] = bad;
     scal[1] = logdet;  // log|V| = Σ log pivots (Step 2)
+    double ldx = 0.0;  // log|XᵀV⁻¹X| = 2 Σ log Q_cc (Step 5, Table 1 detReml)
+    if (!bad)
+      for (int c = 0; c < p; ++c) ldx += 2.0 * log(Q[c * 64 + c]);
+    scal[2] = ldx;
   }
   __syncthreads();
   if (flag[1]) {
@@ -646,7 +661,7 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   }
   const double S = *A.S;
   const double n = (double)g.n;
-  const double ldV = scal[1];
+  const double ldV = scal[1], ldx = scal[2];
   const double ln2pi = 1.8378770664093454836;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   for (int m = tid; m < M; m += NT) {
@@ -668,21 +683,34 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
       bt[a] = s / Q[a * 64 + a];
     }
     const size_t km = (size_t)k * M + m;
+    if (A.ssqBetahat) A.ssqBetahat[km] = sb;
+    if (A.ssqResidual) A.ssqResidual[km] = yy - sb;
     if (neg) {
       A.loglik[km] = -INFINITY;
       A.sigma2hat[km] = nan;
       for (int a = 0; a < p; ++a) A.betahat[km * p + a] = nan;
+      if (A.loglik_reml) A.loglik_reml[km] = -INFINITY;
+      if (A.sigma2hat_reml) A.sigma2hat_reml[km] = nan;
       atomicExch(&flag[2], 1);
     } else {
       const double s2 = q / n;  // Eq. 4
+      const double jac = (A.lambdas[m] - 1.0) * S;
       // Eq. (profile): −2ℓ_p = n log σ̂² + log|V| − 2(λ−1)Σ log y + n log 2π + n
-      A.loglik[km] = -0.5 * (n * log(s2) + ldV + n * ln2pi + n) + (A.lambdas[m] - 1.0) * S;
+      A.loglik[km] = -0.5 * (n * log(s2) + ldV + n * ln2pi + n) + jac;
       A.sigma2hat[km] = s2;
       for (int a = 0; a < p; ++a) A.betahat[km * p + a] = bt[a];
+      if (A.loglik_reml || A.sigma2hat_reml) {
+        // Eq. remlpro with σ̂²_reml = q/(n−p) (Eq. sigmahat_reml_y)
+        const double np_ = n - p, s2r = q / np_;
+        if (A.sigma2hat_reml) A.sigma2hat_reml[km] = s2r;
+        if (A.loglik_reml)
+          A.loglik_reml[km] = -0.5 * (np_ * log(s2r) + ldV + ldx + n * ln2pi + np_) + jac;
+      }
     }
   }
   __syncthreads();
   if (tid == 0) {
+    if (A.detReml) A.detReml[k] = ldx;
     A.logdetV[k] = ldV;
     A.status[k] = flag[2] ? LIK_PT_NEG_RESID : LIK_PT_OK;
   }

@@ -139,9 +139,15 @@ cudaEvent_t ev_get(lik_ctx* c, size_t i) {
 }
 
 // The hot path on device buffers (inputs already validated).
+struct Extras {
+  double *detReml = nullptr, *ssqYX = nullptr, *ssqBetahat = nullptr, *ssqResidual = nullptr,
+         *loglik_reml = nullptr, *sigma2hat_reml = nullptr;
+};
+
 int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, const double* X,
                int K, const double* params, int M, const double* lambdas, double* loglik,
-               double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st) {
+               double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st,
+               const Extras& ex = Extras()) {
   const SlotGeom g = lik::make_geom(n, M + p);
   const size_t slot_bytes = g.slot_d * sizeof(double);
   int W = c->wave_points > 0 ? c->wave_points : c->nsm * lik::chol_ctas_per_sm();
@@ -192,6 +198,12 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     a.sigma2hat = sigma2hat;
     a.logdetV = logdetV;
     a.status = status;
+    a.detReml = ex.detReml;
+    a.ssqYX = ex.ssqYX;
+    a.ssqBetahat = ex.ssqBetahat;
+    a.ssqResidual = ex.ssqResidual;
+    a.loglik_reml = ex.loglik_reml;
+    a.sigma2hat_reml = ex.sigma2hat_reml;
     CUDA_TRY(c, lik::launch_chol(a, kw, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   }
@@ -270,6 +282,17 @@ int lik_eval_batch_device(lik_ctx* c, int n, int p, const double* coords, const 
                           const double* X, int K, const double* params, int M,
                           const double* lambdas, double* loglik, double* betahat,
                           double* sigma2hat, double* logdetV, int* status, void* cuda_stream) {
+  return lik_eval_batch_device_ex(c, n, p, coords, y, X, K, params, M, lambdas, loglik, betahat,
+                                  sigma2hat, logdetV, status, nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, nullptr, cuda_stream);
+}
+
+int lik_eval_batch_device_ex(lik_ctx* c, int n, int p, const double* coords, const double* y,
+                             const double* X, int K, const double* params, int M,
+                             const double* lambdas, double* loglik, double* betahat,
+                             double* sigma2hat, double* logdetV, int* status, double* detReml,
+                             double* ssqYX, double* ssqBetahat, double* ssqResidual,
+                             double* loglik_reml, double* sigma2hat_reml, void* cuda_stream) {
   if (!c) return LIK_EINVAL;
   c->err.clear();
   if (any_null({coords, y, X, params, lambdas, loglik, betahat, sigma2hat, logdetV, status}))
@@ -290,8 +313,15 @@ int lik_eval_batch_device(lik_ctx* c, int n, int p, const double* coords, const 
   CUDA_TRY(c, cudaStreamSynchronize(st));
   int rc = validate(c, n, p, hc, hy, hX, K, M, hl);
   if (rc) return rc;
+  Extras ex;
+  ex.detReml = detReml;
+  ex.ssqYX = ssqYX;
+  ex.ssqBetahat = ssqBetahat;
+  ex.ssqResidual = ssqResidual;
+  ex.loglik_reml = loglik_reml;
+  ex.sigma2hat_reml = sigma2hat_reml;
   return run_device(c, n, p, coords, y, X, K, params, M, lambdas, loglik, betahat, sigma2hat,
-                    logdetV, status, st);
+                    logdetV, status, st, ex);
 }
 
 int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double* y,

@@ -110,6 +110,13 @@ struct CholArgs {
   double* sigma2hat;       // K×M
   double* logdetV;         // K
   int* status;             // K
+  // optional Table-1 / REML outputs (NULL = skip)
+  double* detReml;         // K
+  double* ssqYX;           // K×r×r
+  double* ssqBetahat;      // K×M
+  double* ssqResidual;     // K×M
+  double* loglik_reml;     // K×M
+  double* sigma2hat_reml;  // K×M
 };
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
 size_t chol_smem_bytes();

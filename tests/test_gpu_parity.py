@@ -229,3 +229,29 @@ def test_stage_timing_api():
     c.reset_stage_times()
     assert c.stage_times()["chol_fused"] == (0.0, 0)
     c.close()
+
+
+def test_reml_and_table1_summaries(ctx, orc):
+    """NEXT-1: Table-1 summaries and the REML profile likelihood (Appendix) vs the oracle;
+    the ML outputs of the _ex entry point are bitwise those of lik_eval_batch_device."""
+    for name, K in (("C1", 16), ("C2", 64)):
+        coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
+        t = [torch.tensor(a, device="cuda") for a in (coords, y, X, P, lam)]
+        ex = ctx.eval_batch_device_ex(*t)
+        base = ctx.eval_batch_device(*t)
+        torch.cuda.synchronize()
+        ex = {k: v.cpu().numpy() for k, v in ex.items()}
+        for k2, v in base.items():
+            assert np.array_equal(v.cpu().numpy(), ex[k2], equal_nan=True), k2
+        ref = orc.eval_batch(coords, y, X, P, lam, nthreads=NTHREADS, summaries=True)
+        ok = ref["status"] == 0
+        assert np.array_equal(ex["status"], ref["status"])
+        rel = lambda a, b: np.abs(a - b) / np.maximum(np.abs(b), 1.0)
+        assert rel(ex["detReml"][ok], ref["detReml"][ok]).max() <= 1e-8
+        sc = np.abs(ref["ssqYX"][ok]).max(axis=(1, 2), keepdims=True)
+        assert (np.abs(ex["ssqYX"][ok] - ref["ssqYX"][ok]) / sc).max() <= 1e-8
+        yy = np.stack([np.diagonal(ref["ssqYX"][kk])[:lam.shape[0]] for kk in range(len(P))])[ok]
+        assert (np.abs(ex["ssqBetahat"][ok] - ref["ssqBetahat"][ok]) / yy).max() <= 1e-8
+        assert (np.abs(ex["ssqResidual"][ok] - ref["ssqResidual"][ok]) / yy).max() <= 1e-8
+        assert (np.abs(ex["loglik_reml"][ok] - ref["loglik_reml"][ok]) / np.abs(ref["loglik_reml"][ok])).max() <= 1e-8
+        assert (np.abs(ex["sigma2hat_reml"][ok] - ref["sigma2_reml"][ok]) / ref["sigma2_reml"][ok]).max() <= 1e-8
