@@ -71,6 +71,9 @@ enum {
 
 /* lik_create flags */
 #define LIK_FLAG_TIMING 1u /* record CUDA events around every kernel launch (lik_get_stage_times) */
+#define LIK_FLAG_NATURAL_ORDER 2u /* keep the caller's site order (default: Morton order for the
+                                     Matérn build; results agree to rounding, invariance of ℓ_p
+                                     under a symmetric permutation of the sites) */
 
 /* Stages reported by lik_get_stage_times. */
 enum {

@@ -24,6 +24,7 @@ LIB_PATH = os.environ.get("LIK_LIBRARY") or os.path.join(HERE, "liblik.so")  # L
 LIK_OK, LIK_EINVAL, LIK_EDOMAIN, LIK_ERANK, LIK_ENOMEM, LIK_ECUDA, LIK_ENOTIMPL = 0, -1, -2, -3, -4, -5, -6
 PT_OK, PT_V_NOT_PD, PT_XVX_NOT_PD, PT_NEG_RESID, PT_BAD_PARAM = 0, 1, 2, 3, 4
 FLAG_TIMING = 1
+FLAG_NATURAL_ORDER = 2
 STAGES = ("prep", "setup", "matern_build", "chol_fused")
 ABI_SYMBOLS = ("lik_create", "lik_destroy", "lik_last_error", "lik_eval_batch",
                "lik_eval_batch_device", "lik_get_stage_times", "lik_reset_stage_times",

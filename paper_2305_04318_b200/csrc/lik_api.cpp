@@ -32,6 +32,11 @@ struct lik_ctx {
   double* S = nullptr;
   double* table = nullptr;
   size_t table_bytes = 0;
+  double* coords_p = nullptr;  // sites in Morton order (device)
+  size_t coords_p_bytes = 0;
+  int* perm = nullptr;         // Morton order (device)
+  size_t perm_bytes = 0;
+  std::vector<int> hperm;
   // host-API staging buffers
   char* io = nullptr;
   size_t io_bytes = 0;
@@ -129,6 +134,39 @@ int validate(lik_ctx* c, int n, int p, const double* coords, const double* y, co
   return LIK_OK;
 }
 
+// Site order for the Matérn build: Morton (Z-curve) order of the coordinates, so
+// that consecutive sites are spatial neighbours (locality of the per-warp
+// Chebyshev octaves).  A symmetric permutation of the sites (with y and X rows)
+// leaves V's determinant, the quadratic forms and hence every output unchanged.
+void morton_order(int n, const double* coords, std::vector<int>& perm) {
+  double xmin = coords[0], xmax = coords[0], ymin = coords[1], ymax = coords[1];
+  for (int i = 1; i < n; ++i) {
+    xmin = std::min(xmin, coords[2 * i]);
+    xmax = std::max(xmax, coords[2 * i]);
+    ymin = std::min(ymin, coords[2 * i + 1]);
+    ymax = std::max(ymax, coords[2 * i + 1]);
+  }
+  const double span = std::max(std::max(xmax - xmin, ymax - ymin), 1e-300);
+  auto spread = [](uint64_t v) {
+    v &= 0x1fffff;
+    v = (v | v << 32) & 0x1f00000000ffffULL;
+    v = (v | v << 16) & 0x1f0000ff0000ffULL;
+    v = (v | v << 8) & 0x100f00f00f00f00fULL;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+    v = (v | v << 2) & 0x1249249249249249ULL;
+    return v;
+  };
+  std::vector<std::pair<uint64_t, int>> key(n);
+  for (int i = 0; i < n; ++i) {
+    const uint64_t qx = (uint64_t)((coords[2 * i] - xmin) / span * 2097151.0);
+    const uint64_t qy = (uint64_t)((coords[2 * i + 1] - ymin) / span * 2097151.0);
+    key[i] = {spread(qx) | (spread(qy) << 1), i};
+  }
+  std::sort(key.begin(), key.end());
+  perm.resize(n);
+  for (int i = 0; i < n; ++i) perm[i] = key[i].second;
+}
+
 cudaEvent_t ev_get(lik_ctx* c, size_t i) {
   while (c->ev.size() <= i) {
     cudaEvent_t e;
@@ -147,7 +185,7 @@ struct Extras {
 int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, const double* X,
                int K, const double* params, int M, const double* lambdas, double* loglik,
                double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st,
-               const Extras& ex = Extras()) {
+               const double* hcoords, const Extras& ex = Extras()) {
   const SlotGeom g = lik::make_geom(n, M + p);
   const size_t slot_bytes = g.slot_d * sizeof(double);
   int W = c->wave_points > 0 ? c->wave_points : c->nsm * lik::chol_ctas_per_sm();
@@ -171,18 +209,29 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)W * lik::TABLE_D * sizeof(double))))
     return rc;
 
+  if ((rc = ensure(c, &c->coords_p, &c->coords_p_bytes, (size_t)n * 2 * sizeof(double)))) return rc;
+  const int* dperm = nullptr;
+  if (!(c->flags & LIK_FLAG_NATURAL_ORDER)) {
+    morton_order(n, hcoords, c->hperm);
+    if ((rc = ensure(c, &c->perm, &c->perm_bytes, (size_t)n * sizeof(int)))) return rc;
+    CUDA_TRY(c, cudaMemcpyAsync(c->perm, c->hperm.data(), (size_t)n * sizeof(int),
+                                cudaMemcpyHostToDevice, st));
+    dperm = c->perm;
+  }
+
   const bool timing = c->flags & LIK_FLAG_TIMING;
   const int nwaves = (K + W - 1) / W;
   size_t ei = 0;
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
-  CUDA_TRY(c, lik::launch_prep(y, X, lambdas, n, p, M, g.nt * lik::TB, c->bt, c->S, st));
+  CUDA_TRY(c, lik::launch_prep(coords, y, X, lambdas, dperm, n, p, M, g.nt * lik::TB, c->coords_p,
+                               c->bt, c->S, st));
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   for (int w = 0; w < nwaves; ++w) {
     const int k0 = w * W, kw = std::min(W, K - k0);
     CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, st));
-    CUDA_TRY(c, lik::launch_build(coords, g, c->pc, k0, kw, c->table, c->bt, c->ws, st));
+    CUDA_TRY(c, lik::launch_build(c->coords_p, g, c->pc, k0, kw, c->table, c->bt, c->ws, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
     a.ws = c->ws;
@@ -241,7 +290,7 @@ extern "C" {
 int lik_create(lik_ctx** out, int cuda_device, unsigned flags) {
   if (!out) return LIK_EINVAL;
   *out = nullptr;
-  if (flags & ~LIK_FLAG_TIMING) return LIK_EINVAL;
+  if (flags & ~(LIK_FLAG_TIMING | LIK_FLAG_NATURAL_ORDER)) return LIK_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
     return LIK_ECUDA;
@@ -270,6 +319,8 @@ void lik_destroy(lik_ctx* c) {
   cudaFree(c->bt);
   cudaFree(c->S);
   cudaFree(c->table);
+  cudaFree(c->coords_p);
+  cudaFree(c->perm);
   cudaFree(c->io);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -321,7 +372,7 @@ int lik_eval_batch_device_ex(lik_ctx* c, int n, int p, const double* coords, con
   ex.loglik_reml = loglik_reml;
   ex.sigma2hat_reml = sigma2hat_reml;
   return run_device(c, n, p, coords, y, X, K, params, M, lambdas, loglik, betahat, sigma2hat,
-                    logdetV, status, st, ex);
+                    logdetV, status, st, hc, ex);
 }
 
 int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double* y,
@@ -358,7 +409,7 @@ int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double*
   CUDA_TRY(c, cudaMemcpyAsync(dX, X, (size_t)n * p * 8, cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(dp, params, (size_t)K * 5 * 8, cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(dl, lambdas, (size_t)M * 8, cudaMemcpyHostToDevice, st));
-  rc = run_device(c, n, p, dc, dy, dX, K, dp, M, dl, dll, dbh, ds2, dld, dst, st);
+  rc = run_device(c, n, p, dc, dy, dX, K, dp, M, dl, dll, dbh, ds2, dld, dst, st, coords);
   if (rc) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(loglik, dll, (size_t)K * M * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaMemcpyAsync(betahat, dbh, (size_t)K * M * p * 8, cudaMemcpyDeviceToHost, st));

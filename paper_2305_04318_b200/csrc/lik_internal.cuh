@@ -87,8 +87,11 @@ constexpr int CHEB_NOCT = 40;
 constexpr int TABLE_D = CHEB_STRIDE * CHEB_NOCT;
 
 // Launch wrappers (defined in the .cu files).  All enqueue on `st`.
-cudaError_t launch_prep(const double* y, const double* X, const double* lambdas, int n, int p,
-                        int M, int npad, double* Bt, double* S, cudaStream_t st);
+// prep: Box-Cox rows of Bᵀ, S = Σ log y, and the site gather coords_p[i] = coords[perm[i]]
+// (perm == nullptr: identity).
+cudaError_t launch_prep(const double* coords, const double* y, const double* X,
+                        const double* lambdas, const int* perm, int n, int p, int M, int npad,
+                        double* coords_p, double* Bt, double* S, cudaStream_t st);
 cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st);
 cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, cudaStream_t st);
 cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,

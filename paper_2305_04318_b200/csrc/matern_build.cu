@@ -10,31 +10,38 @@
 namespace lik {
 
 // ---------------------------------------------------------------------------
-// prep: grid = r + 1 blocks.  Block t < r writes row t of Bᵀ (r × npad,
-// zero-padded); block r computes S = Σ log y_i with a fixed-order reduction.
+// prep: grid = r + 2 blocks.  Block t < r writes row t of Bᵀ (r × npad,
+// zero-padded); block r computes S = Σ log y_i with a fixed-order reduction;
+// block r + 1 gathers the (possibly reordered) site coordinates.  Sites are
+// taken in the order perm (Morton order chosen by the host for locality of the
+// Matérn build); the likelihood is invariant under a symmetric permutation of
+// the sites (with y and X rows).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ y,
+__global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ coords,
+                                                   const double* __restrict__ y,
                                                    const double* __restrict__ X,
-                                                   const double* __restrict__ lambdas, int n,
-                                                   int p, int M, int npad, double* __restrict__ Bt,
-                                                   double* __restrict__ S) {
+                                                   const double* __restrict__ lambdas,
+                                                   const int* __restrict__ perm, int n, int p, int M,
+                                                   int npad, double* __restrict__ coords_p,
+                                                   double* __restrict__ Bt, double* __restrict__ S) {
   const int t = blockIdx.x;
   const int r = M + p;
   if (t < r) {
     for (int i = threadIdx.x; i < npad; i += blockDim.x) {
       double v = 0.0;
       if (i < n) {
+        const int src = perm ? perm[i] : i;
         if (t < M) {
           const double lam = lambdas[t];
-          const double ly = log(y[i]);
+          const double ly = log(y[src]);
           v = (fabs(lam) < 1e-10) ? ly : expm1(lam * ly) / lam;
         } else {
-          v = X[(size_t)i * p + (t - M)];
+          v = X[(size_t)src * p + (t - M)];
         }
       }
       Bt[(size_t)t * npad + i] = v;
     }
-  } else {
+  } else if (t == r) {
     __shared__ double red[256];
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += 256) s += log(y[i]);
@@ -45,12 +52,19 @@ __global__ void __launch_bounds__(256) prep_kernel(const double* __restrict__ y,
       __syncthreads();
     }
     if (threadIdx.x == 0) *S = red[0];
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int src = perm ? perm[i] : i;
+      coords_p[2 * i] = coords[2 * src];
+      coords_p[2 * i + 1] = coords[2 * src + 1];
+    }
   }
 }
 
-cudaError_t launch_prep(const double* y, const double* X, const double* lambdas, int n, int p,
-                        int M, int npad, double* Bt, double* S, cudaStream_t st) {
-  prep_kernel<<<M + p + 1, 256, 0, st>>>(y, X, lambdas, n, p, M, npad, Bt, S);
+cudaError_t launch_prep(const double* coords, const double* y, const double* X,
+                        const double* lambdas, const int* perm, int n, int p, int M, int npad,
+                        double* coords_p, double* Bt, double* S, cudaStream_t st) {
+  prep_kernel<<<M + p + 2, 256, 0, st>>>(coords, y, X, lambdas, perm, n, p, M, npad, coords_p, Bt, S);
   return cudaGetLastError();
 }
 
@@ -191,30 +205,17 @@ cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, cudaStre
 // written as 0).  Padded rows/columns (index ≥ n) hold the identity, which
 // leaves log|V| and L⁻¹B unchanged.  Augmented tile j holds Bᵀ[:, 64j:64j+64].
 // ---------------------------------------------------------------------------
+constexpr int BUILD_TILES = 4;  // tiles of one point per block (amortises the table load)
+
 __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ coords, SlotGeom g,
                                                     const PointConst* __restrict__ pc, int k0,
                                                     const double* __restrict__ table,
                                                     const double* __restrict__ Bt,
                                                     double* __restrict__ ws) {
-  const int tile = blockIdx.x;
   const int slot = blockIdx.y;
   const PointConst P = pc[k0 + slot];
   if (P.mode == MODE_BAD) return;
-  double* T = ws + (size_t)slot * g.slot_d + (size_t)tile * TILE_D;
   const int npad = g.nt * TB;
-  if (tile >= g.ntri) {
-    const int j = tile - g.ntri;
-    for (int e = threadIdx.x; e < TILE_D; e += 256) {
-      const int r = e >> 6, c = e & 63;
-      T[sw_off(r, c)] = (r < g.r) ? Bt[(size_t)r * npad + j * TB + c] : 0.0;
-    }
-    return;
-  }
-  // tile (i, j) from the packed index
-  int i = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
-  while (tri_index(i + 1, 0) <= tile) ++i;
-  while (tri_index(i, 0) > tile) --i;
-  const int j = tile - tri_index(i, 0);
   __shared__ double sx[2][TB], sy[2][TB];
   __shared__ double coef[TABLE_D];
   if (P.mode == MODE_BESSEL) {
@@ -222,60 +223,78 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
     const int nval = min(CHEB_NOCT, max(0, P.e_zero - CHEB_ELO)) * CHEB_STRIDE;
     for (int e = threadIdx.x; e < nval; e += 256) coef[e] = src[e];
   }
-  if (threadIdx.x < TB) {
-    const int gi = i * TB + threadIdx.x;
-    sx[0][threadIdx.x] = gi < g.n ? coords[2 * gi] : 0.0;
-    sy[0][threadIdx.x] = gi < g.n ? coords[2 * gi + 1] : 0.0;
-  } else if (threadIdx.x < 2 * TB) {
-    const int gj = j * TB + threadIdx.x - TB;
-    sx[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj] : 0.0;
-    sy[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj + 1] : 0.0;
-  }
-  __syncthreads();
-  // thread -> column c, rows r0 + 4q (q < 16): the warp covers 32 consecutive
-  // columns of one row, so stores are coalesced and the table reads of a warp
-  // mostly hit the same octave.
+  // thread -> column c, rows r0 + 4q (q < 16): a warp covers 32 consecutive
+  // columns of one row; with Morton-ordered sites their z values mostly share an
+  // octave, so the coefficient loads are shared-memory broadcasts.
   const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
-  const double xj = sx[1][c], yj = sy[1][c];
-  // all elements of the tile are off-diagonal Matérn values (no padding / diagonal)?
-  const bool regular = (i > j) && ((i + 1) * TB <= g.n);
-  unsigned slow = 0u;
-  if (P.mode == MODE_BESSEL) {
-#pragma unroll 2
-    for (int q = 0; q < 16; q += 2) {
-      const int ra = r0 + 4 * q, rb = ra + 4;
-      double va, vb;
-      matern_rho_table2(P, coef, sx[0][ra] - xj, sy[0][ra] - yj, sx[0][rb] - xj, sy[0][rb] - yj,
-                        va, vb, slow, q);
-      T[sw_off(ra, c)] = va;
-      T[sw_off(rb, c)] = vb;
-    }
-  } else {
-#pragma unroll 4
-    for (int q = 0; q < 16; ++q) {
-      const int ra = r0 + 4 * q;
-      T[sw_off(ra, c)] = exp(-2.0 * aniso_d2(P, sx[0][ra] - xj, sy[0][ra] - yj));
-    }
-  }
-  if (!regular || slow) {
-    // fix-up pass (rewrites): padding, diagonal, unused upper triangle, outside the table
-#pragma unroll 1
-    for (int q = 0; q < 16; ++q) {
-      const int r = r0 + 4 * q;
-      const int gi = i * TB + r, gj = j * TB + c;
-      double v;
-      if (gi >= g.n || gj >= g.n) {
-        v = (gi == gj) ? 1.0 : 0.0;
-      } else if (gi == gj) {
-        v = 1.0 + P.nugget;
-      } else if (i == j && c > r) {
-        v = 0.0;
-      } else if ((slow >> q) & 1u) {
-        v = matern_rho_exact(P, sx[0][r] - xj, sy[0][r] - yj);
-      } else {
-        continue;
+  for (int tt = 0; tt < BUILD_TILES; ++tt) {
+    const int tile = blockIdx.x * BUILD_TILES + tt;
+    if (tile >= g.ntri + g.nt) break;
+    double* T = ws + (size_t)slot * g.slot_d + (size_t)tile * TILE_D;
+    if (tile >= g.ntri) {
+      const int j = tile - g.ntri;
+      for (int e = threadIdx.x; e < TILE_D; e += 256) {
+        const int r = e >> 6, cc = e & 63;
+        T[sw_off(r, cc)] = (r < g.r) ? Bt[(size_t)r * npad + j * TB + cc] : 0.0;
       }
-      T[sw_off(r, c)] = v;
+      continue;
+    }
+    // tile (i, j) from the packed index
+    int i = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+    while (tri_index(i + 1, 0) <= tile) ++i;
+    while (tri_index(i, 0) > tile) --i;
+    const int j = tile - tri_index(i, 0);
+    __syncthreads();  // previous tile's coordinates are no longer read
+    if (threadIdx.x < TB) {
+      const int gi = i * TB + threadIdx.x;
+      sx[0][threadIdx.x] = gi < g.n ? coords[2 * gi] : 0.0;
+      sy[0][threadIdx.x] = gi < g.n ? coords[2 * gi + 1] : 0.0;
+    } else if (threadIdx.x < 2 * TB) {
+      const int gj = j * TB + threadIdx.x - TB;
+      sx[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj] : 0.0;
+      sy[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj + 1] : 0.0;
+    }
+    __syncthreads();
+    const double xj = sx[1][c], yj = sy[1][c];
+    const bool regular = (i > j) && ((i + 1) * TB <= g.n);
+    unsigned slow = 0u;
+    if (P.mode == MODE_BESSEL) {
+#pragma unroll 2
+      for (int q = 0; q < 16; q += 2) {
+        const int ra = r0 + 4 * q, rb = ra + 4;
+        double va, vb;
+        matern_rho_table2(P, coef, sx[0][ra] - xj, sy[0][ra] - yj, sx[0][rb] - xj, sy[0][rb] - yj,
+                          va, vb, slow, q);
+        T[sw_off(ra, c)] = va;
+        T[sw_off(rb, c)] = vb;
+      }
+    } else {
+#pragma unroll 4
+      for (int q = 0; q < 16; ++q) {
+        const int ra = r0 + 4 * q;
+        T[sw_off(ra, c)] = exp(-2.0 * aniso_d2(P, sx[0][ra] - xj, sy[0][ra] - yj));
+      }
+    }
+    if (!regular || slow) {
+      // fix-up pass (rewrites): padding, diagonal, unused upper triangle, outside the table
+#pragma unroll 1
+      for (int q = 0; q < 16; ++q) {
+        const int r = r0 + 4 * q;
+        const int gi = i * TB + r, gj = j * TB + c;
+        double v;
+        if (gi >= g.n || gj >= g.n) {
+          v = (gi == gj) ? 1.0 : 0.0;
+        } else if (gi == gj) {
+          v = 1.0 + P.nugget;
+        } else if (i == j && c > r) {
+          v = 0.0;
+        } else if ((slow >> q) & 1u) {
+          v = matern_rho_exact(P, sx[0][r] - xj, sy[0][r] - yj);
+        } else {
+          continue;
+        }
+        T[sw_off(r, c)] = v;
+      }
     }
   }
 }
@@ -283,7 +302,7 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
 cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
                          int kw, const double* table, const double* Bt, double* ws,
                          cudaStream_t st) {
-  dim3 grid(g.ntri + g.nt, kw);
+  dim3 grid((g.ntri + g.nt + BUILD_TILES - 1) / BUILD_TILES, kw);
   build_kernel<<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
   return cudaGetLastError();
 }

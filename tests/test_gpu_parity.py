@@ -255,3 +255,16 @@ def test_reml_and_table1_summaries(ctx, orc):
         assert (np.abs(ex["ssqResidual"][ok] - ref["ssqResidual"][ok]) / yy).max() <= 1e-8
         assert (np.abs(ex["loglik_reml"][ok] - ref["loglik_reml"][ok]) / np.abs(ref["loglik_reml"][ok])).max() <= 1e-8
         assert (np.abs(ex["sigma2hat_reml"][ok] - ref["sigma2_reml"][ok]) / ref["sigma2_reml"][ok]).max() <= 1e-8
+
+
+def test_site_order_invariance():
+    """The default Morton site order and the caller's natural order give the same
+    likelihoods (a symmetric permutation of V leaves |V| and the quadratic forms
+    unchanged; only the rounding order differs)."""
+    coords, y, X, P, lam = synthgen.make_inputs("C2", K=48)
+    a = lik.create(0).eval_batch(coords, y, X, P, lam)
+    b = lik.create(0, lik.FLAG_NATURAL_ORDER).eval_batch(coords, y, X, P, lam)
+    assert np.array_equal(a["status"], b["status"])
+    np.testing.assert_allclose(a["loglik"], b["loglik"], rtol=1e-11)
+    np.testing.assert_allclose(a["logdetV"], b["logdetV"], rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(a["betahat"], b["betahat"], rtol=1e-9, atol=1e-9 * np.abs(a["betahat"]).max())
