@@ -58,6 +58,9 @@ def lib():
         L.oracle_eval.restype = _I
         L.oracle_eval.argtypes = [_I, _I, _PD, _PD, _PD, _I, _PD, _I, _PD,
                                   _PD, _PD, _PD, _PD, _PI, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _I]
+        L.oracle_profiles.restype = None
+        L.oracle_profiles.argtypes = [_I, _I, _I, _I, _PD, _PD, _PI, _PD, _PD, _I, _PD, _PD, _I,
+                                      _PD, _PD, _PD]
         _lib = L
     return _lib
 
@@ -148,3 +151,17 @@ def eval_batch(coords, y, X, params, lambdas, nthreads: int | None = None, summa
         _p(out["sigma2_reml"]) if summaries else nul, int(nt))
     out["rc"] = rc
     return out
+
+
+def profiles(n, p, ssqYX, logdetV, status, lambdas, y, beta_grid, sigma_grid):
+    """β_a, σ and λ profile log-likelihoods over the K×M grid from summaries.
+    Returns (prof_beta p×G, prof_sigma Sg, prof_lambda M)."""
+    ssqYX, logdetV, lambdas, y = map(_c, (ssqYX, logdetV, lambdas, y))
+    status = np.ascontiguousarray(status, dtype=np.int32)
+    beta_grid = _c(beta_grid).reshape(p, -1)
+    sigma_grid = _c(sigma_grid)
+    K, M, G, Sg = logdetV.shape[0], lambdas.shape[0], beta_grid.shape[1], sigma_grid.shape[0]
+    ob, os_, ol = np.empty((p, G)), np.empty(Sg), np.empty(M)
+    lib().oracle_profiles(n, p, K, M, _p(ssqYX), _p(logdetV), status.ctypes.data_as(_PI), _p(lambdas),
+                          _p(y), G, _p(beta_grid), _p(ob), Sg, _p(sigma_grid), _p(os_), _p(ol))
+    return ob, os_, ol

@@ -410,4 +410,98 @@ int oracle_eval(int n, int p, const double* coords, const double* y, const doubl
   return OK;
 }
 
+// ---------------------------------------------------------------------------
+// Profile log-likelihoods over the K×M grid (§3.4-3.6), from the Table-1
+// summaries (the caller passes the oracle's own ssqYX, logdetV, status).
+//  β_a profile (Eq. profilebetai): for β_a = b,
+//    Q0 = y'ᵀV⁻¹y' − 2b (XᵀV⁻¹y')_a + b² (XᵀV⁻¹X)_aa
+//    T  = (g0 − b g1)ᵀ H⁻¹ (g0 − b g1),  H = (XᵀV⁻¹X)_[−a,−a],
+//         g0 = (XᵀV⁻¹y')_[−a], g1 = (XᵀV⁻¹X)_[−a,a]
+//    q(b) = Q0 − T;  ℓ = −½[n log(q/n) + log|V| + n log 2π + n] + (λ−1)S,
+//    out_beta[a·G + g] = max over (k, m) of ℓ at b = beta_grid[a·G + g].
+//  σ profile (Eq. profileSigma): with q = ssqResidual (β̂ profiled),
+//    ℓ(σ) = −½[q/σ² + n log σ² + log|V| + n log 2π] + (λ−1)S, max over (k, m).
+//  λ profile: out_lambda[m] = max over k of ℓ_p(ω_k, λ_m).
+// ---------------------------------------------------------------------------
+void oracle_profiles(int n, int p, int K, int M, const double* ssqYX, const double* logdetV,
+                     const int* status, const double* lambdas, const double* y, int G,
+                     const double* beta_grid, double* out_beta, int Sg,
+                     const double* sigma_grid, double* out_sigma, double* out_lambda) {
+  const int r = M + p;
+  double S = 0.0;
+  for (int i = 0; i < n; ++i) S += std::log(y[i]);
+  const double ln2pi = std::log(2.0 * kPi);
+  for (int e = 0; e < p * G; ++e) out_beta[e] = -INFINITY;
+  for (int e = 0; e < Sg; ++e) out_sigma[e] = -INFINITY;
+  for (int m = 0; m < M; ++m) out_lambda[m] = -INFINITY;
+  for (int k = 0; k < K; ++k) {
+    if (status[k] != 0) continue;
+    const double* C = ssqYX + (size_t)k * r * r;
+    auto c = [&](int i, int j) { return C[(size_t)i * r + j]; };
+    // full XᵀV⁻¹X factor for β̂ (σ and λ profiles)
+    std::vector<double> XX((size_t)p * p), Dx(p);
+    for (int a = 0; a < p; ++a)
+      for (int b = 0; b < p; ++b) XX[(size_t)a * p + b] = c(M + a, M + b);
+    if (ldl(p, XX.data(), Dx.data())) continue;
+    for (int m = 0; m < M; ++m) {
+      const double jac = (lambdas[m] - 1.0) * S;
+      // q = y'ᵀV⁻¹y' − (XᵀV⁻¹y')ᵀ(XᵀV⁻¹X)⁻¹(XᵀV⁻¹y')  (Step 8)
+      std::vector<double> xy(p), u(p);
+      for (int a = 0; a < p; ++a) xy[a] = c(M + a, m);
+      forward_unit(p, XX.data(), 1, xy.data(), u.data());
+      double sb = 0.0;
+      for (int a = 0; a < p; ++a) sb += u[a] * u[a] / Dx[a];
+      const double q = c(m, m) - sb;
+      const double lp = -0.5 * (n * std::log(q / n) + logdetV[k] + n * ln2pi + n) + jac;
+      out_lambda[m] = std::max(out_lambda[m], lp);
+      for (int t = 0; t < Sg; ++t) {
+        const double s2 = sigma_grid[t] * sigma_grid[t];
+        const double l = -0.5 * (q / s2 + n * std::log(s2) + logdetV[k] + n * ln2pi) + jac;
+        out_sigma[t] = std::max(out_sigma[t], l);
+      }
+      for (int a = 0; a < p; ++a) {
+        // H = (XᵀV⁻¹X) without row/column a, g0, g1
+        const int pm = p - 1;
+        std::vector<double> H((size_t)pm * pm + 1), Dh(pm + 1), g0(pm + 1), g1(pm + 1);
+        std::vector<double> w0(pm + 1), w1(pm + 1);
+        int ii = 0;
+        for (int i = 0; i < p; ++i) {
+          if (i == a) continue;
+          int jj = 0;
+          for (int j = 0; j < p; ++j) {
+            if (j == a) continue;
+            H[(size_t)ii * pm + jj] = c(M + i, M + j);
+            ++jj;
+          }
+          g0[ii] = c(M + i, m);
+          g1[ii] = c(M + i, M + a);
+          ++ii;
+        }
+        bool okH = true;
+        if (pm > 0) {
+          okH = ldl(pm, H.data(), Dh.data()) == 0;
+          forward_unit(pm, H.data(), 1, g0.data(), w0.data());
+          forward_unit(pm, H.data(), 1, g1.data(), w1.data());
+        }
+        if (!okH) continue;
+        double t00 = 0.0, t01 = 0.0, t11 = 0.0;  // g0ᵀH⁻¹g0, g0ᵀH⁻¹g1, g1ᵀH⁻¹g1
+        for (int i = 0; i < pm; ++i) {
+          t00 += w0[i] * w0[i] / Dh[i];
+          t01 += w0[i] * w1[i] / Dh[i];
+          t11 += w1[i] * w1[i] / Dh[i];
+        }
+        for (int gg = 0; gg < G; ++gg) {
+          const double b = beta_grid[(size_t)a * G + gg];
+          const double Q0 = c(m, m) - 2.0 * b * c(M + a, m) + b * b * c(M + a, M + a);
+          const double T = t00 - 2.0 * b * t01 + b * b * t11;
+          const double qb = Q0 - T;
+          const double l = -0.5 * (n * std::log(qb / n) + logdetV[k] + n * ln2pi + n) + jac;
+          double& o = out_beta[(size_t)a * G + gg];
+          o = std::max(o, l);
+        }
+      }
+    }
+  }
+}
+
 }  // extern "C"

@@ -498,3 +498,78 @@ def test_reml_searle_identities(orc):
         # ssqYX blocks (Table 1): y'ᵀV⁻¹y' on the diagonal, XᵀV⁻¹X lower-right, XᵀV⁻¹y' lower-left
         B = np.column_stack([(y ** l - 1) / l for l in lam] + [X])
         np.testing.assert_allclose(out["ssqYX"][0], B.T @ np.linalg.solve(V, B), rtol=1e-10)
+
+
+# --------------------------------------------------------------------------- profiles (§3.4-3.6)
+def _closed_form_case(K=3, M=2, seed=5):
+    """C1 sites, κ = 3/2 closed-form V (no Bessel) for an independent brute force."""
+    coords, y, X = synthgen.make_dataset("C1")
+    rng = np.random.default_rng(seed)
+    P = np.column_stack([rng.uniform(500, 1500, K), np.full(K, 1.5), rng.uniform(0.1, 0.8, K),
+                         np.ones(K), np.zeros(K)])
+    lam = np.linspace(0.3, 0.7, M)
+    return coords, y, X, P, lam
+
+
+def _V32(coords, w):
+    D = np.sqrt(((coords[:, None, :] - coords[None, :, :]) ** 2).sum(-1)) / w[0]
+    z = math.sqrt(12) * D
+    return (1 + z) * np.exp(-z) + w[2] * np.eye(len(coords))
+
+
+def test_beta_profile_vs_direct_maximisation(orc):
+    """ℓ_p(β_a = b) equals max over (k, m) of the full log-likelihood Eq. 2
+    maximised numerically over β_{−a} and σ² at β_a = b (scipy, explicit V)."""
+    import scipy.optimize as so
+    coords, y, X, P, lam = _closed_form_case()
+    n, p = X.shape
+    out = orc.eval_batch(coords, y, X, P, lam, summaries=True)
+    bh = out["betahat"][0, 0]
+    grid = np.stack([v + np.array([-0.3, 0.05, 0.4]) * max(1.0, abs(v)) for v in bh])
+    prof, _, _ = orc.profiles(n, p, out["ssqYX"], out["logdetV"], out["status"], lam, y, grid, [1.0])
+    for a in range(p):
+        for g, b in enumerate(grid[a]):
+            best = -np.inf
+            for k in range(len(P)):
+                V = _V32(coords, P[k])
+                Vi = np.linalg.inv(V)
+                ld = np.linalg.slogdet(V)[1]
+                for m, l in enumerate(lam):
+                    yp = (y ** l - 1) / l
+                    keep = [i for i in range(p) if i != a]
+
+                    def nll(th):
+                        beta = np.empty(p)
+                        beta[a] = b
+                        beta[keep] = th[:-1]
+                        s2 = math.exp(th[-1])
+                        r = yp - X @ beta
+                        return 0.5 * (r @ Vi @ r / s2 + n * math.log(s2) + ld + n * math.log(2 * math.pi)) \
+                            - (l - 1) * np.log(y).sum()
+                    x0 = np.append(bh[keep], math.log(out["sigma2hat"][k, m]))
+                    res = so.minimize(nll, x0, method="BFGS", options=dict(gtol=1e-10))
+                    best = max(best, -res.fun)
+            assert prof[a, g] == pytest.approx(best, rel=1e-7, abs=1e-7)
+
+
+def test_sigma_and_lambda_profiles(orc):
+    """σ profile vs the scipy multivariate-normal density at (β̂, σ²V) maximised
+    over the grid; λ profile = max_k ℓ_p(ω_k, λ_m); both peak at the global maximum."""
+    coords, y, X, P, lam = _closed_form_case(K=2, M=3)
+    n, p = X.shape
+    out = orc.eval_batch(coords, y, X, P, lam, summaries=True)
+    sig = np.array([0.5, 1.0, 2.0, float(np.sqrt(out["sigma2hat"][0, 1]))])
+    _, ps, pl = orc.profiles(n, p, out["ssqYX"], out["logdetV"], out["status"], lam, y,
+                             np.zeros((p, 1)), sig)
+    np.testing.assert_allclose(pl, out["loglik"].max(axis=0), rtol=1e-12)
+    for t, s in enumerate(sig):
+        best = -np.inf
+        for k in range(len(P)):
+            V = _V32(coords, P[k])
+            for m, l in enumerate(lam):
+                yp = (y ** l - 1) / l
+                ll = sst.multivariate_normal(mean=X @ out["betahat"][k, m], cov=s * s * V).logpdf(yp) \
+                    + (l - 1) * np.log(y).sum()
+                best = max(best, ll)
+        assert ps[t] == pytest.approx(best, rel=1e-10)
+    assert ps.max() <= out["loglik"].max() + 1e-9
