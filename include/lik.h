@@ -136,6 +136,25 @@ int lik_eval_batch_device_ex(lik_ctx* ctx, int n, int p, const double* coords, c
                              double* ssqYX, double* ssqBetahat, double* ssqResidual,
                              double* loglik_reml, double* sigma2hat_reml, void* cuda_stream);
 
+/* Profile log-likelihoods over the K×M grid of evaluated points (SURVEY §8(f)
+ * NEXT-2; §3.4-3.6), from the summaries of lik_eval_batch_device_ex.
+ * All pointers are device pointers; the call is enqueued on `cuda_stream`.
+ *   y          n      the response (Jacobian term Σ log y)
+ *   ssqYX      K×r×r  Table-1 cross products, r = M + p;  logdetV K;  status K
+ *              (points with status != 0 are skipped);  lambdas M
+ *   beta_grid  p×G    values b of each coefficient β_a;  prof_beta p×G:
+ *              ℓ_p(β_a = b) = max over (k, m) of ℓ with β_{−a}, σ² profiled out
+ *              (Eq. profilebetai)
+ *   sigma_grid Sg     values of σ;  prof_sigma Sg: max over (k, m) of ℓ(σ, β̂)
+ *              (Eq. profileSigma)
+ *   prof_lambda M     max over k of ℓ_p(ω_k, λ_m)
+ * Limits: 1 ≤ p ≤ 32, G ≥ 0, Sg ≥ 0.  Returns LIK_OK, LIK_EINVAL, LIK_ENOMEM, LIK_ECUDA. */
+int lik_profiles_device(lik_ctx* ctx, int n, int p, int K, int M, const double* y,
+                        const double* ssqYX, const double* logdetV, const int* status,
+                        const double* lambdas, int G, const double* beta_grid, double* prof_beta,
+                        int Sg, const double* sigma_grid, double* prof_sigma, double* prof_lambda,
+                        void* cuda_stream);
+
 /* Accumulated per-stage device time (ms, from CUDA events on the launching
  * stream) and launch counts since the last reset; arrays of LIK_NSTAGES.
  * Requires LIK_FLAG_TIMING (else LIK_EINVAL). */

@@ -28,7 +28,8 @@ FLAG_NATURAL_ORDER = 2
 STAGES = ("prep", "setup", "matern_build", "chol_fused")
 ABI_SYMBOLS = ("lik_create", "lik_destroy", "lik_last_error", "lik_eval_batch",
                "lik_eval_batch_device", "lik_get_stage_times", "lik_reset_stage_times",
-               "lik_set_wave_points", "lik_debug_build_V", "lik_eval_batch_device_ex")
+               "lik_set_wave_points", "lik_debug_build_V", "lik_eval_batch_device_ex",
+               "lik_profiles_device")
 
 _lib = None
 _PD = ctypes.POINTER(ctypes.c_double)
@@ -63,6 +64,9 @@ def lib():
         L.lik_eval_batch_device.restype = i
         L.lik_eval_batch_device_ex.argtypes = sig + [_VP] * 6 + [_VP]
         L.lik_eval_batch_device_ex.restype = i
+        L.lik_profiles_device.argtypes = [_VP, i, i, i, i, _VP, _VP, _VP, _VP, _VP, i, _VP, _VP, i,
+                                          _VP, _VP, _VP, _VP]
+        L.lik_profiles_device.restype = i
         L.lik_get_stage_times.argtypes = [_VP, _PD, ctypes.POINTER(ctypes.c_longlong)]
         L.lik_get_stage_times.restype = i
         L.lik_reset_stage_times.argtypes = [_VP]
@@ -191,6 +195,25 @@ class Ctx:
             _tptr(out["sigma2hat_reml"]), ctypes.c_void_p(stream.cuda_stream))
         self._check(rc)
         return out
+
+    def profiles_device(self, n, y, summ, lambdas, beta_grid, sigma_grid, stream=None):
+        """lik_profiles_device: β_a, σ and λ profile log-likelihoods from the
+        summaries `summ` of eval_batch_device_ex (torch CUDA tensors)."""
+        import torch
+        p = summ["betahat"].shape[2]
+        K, M = summ["logdetV"].shape[0], lambdas.shape[0]
+        beta_grid = beta_grid.reshape(p, -1).contiguous()
+        G, Sg = beta_grid.shape[1], sigma_grid.shape[0]
+        f = dict(dtype=torch.float64, device=y.device)
+        pb, ps, pl = torch.empty((p, G), **f), torch.empty(max(Sg, 1), **f), torch.empty(M, **f)
+        if stream is None:
+            stream = torch.cuda.current_stream(y.device)
+        rc = lib().lik_profiles_device(
+            self._h, n, p, K, M, _tptr(y), _tptr(summ["ssqYX"]), _tptr(summ["logdetV"]),
+            _tptr(summ["status"]), _tptr(lambdas), G, _tptr(beta_grid), _tptr(pb), Sg,
+            _tptr(sigma_grid), _tptr(ps), _tptr(pl), ctypes.c_void_p(stream.cuda_stream))
+        self._check(rc)
+        return pb, ps[:Sg], pl
 
     def debug_build_V(self, coords, params):
         import torch

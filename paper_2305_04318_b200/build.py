@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblik.so")
-SOURCES = ["lik_api.cpp", "matern_build.cu", "chol_fused.cu"]
+SOURCES = ["lik_api.cpp", "matern_build.cu", "chol_fused.cu", "profiles.cu"]
 HEADERS = ["lik_internal.cuh", "bessel_k.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -35,6 +35,8 @@ struct lik_ctx {
   double* coords_p = nullptr;  // sites in Morton order (device)
   size_t coords_p_bytes = 0;
   int* perm = nullptr;         // Morton order (device)
+  double* prof_scratch = nullptr;  // profile coefficients (lik_profiles_device)
+  size_t prof_scratch_bytes = 0;
   size_t perm_bytes = 0;
   std::vector<int> hperm;
   // host-API staging buffers
@@ -321,6 +323,7 @@ void lik_destroy(lik_ctx* c) {
   cudaFree(c->table);
   cudaFree(c->coords_p);
   cudaFree(c->perm);
+  cudaFree(c->prof_scratch);
   cudaFree(c->io);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -417,6 +420,32 @@ int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double*
   CUDA_TRY(c, cudaMemcpyAsync(logdetV, dld, (size_t)K * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaMemcpyAsync(status, dst, (size_t)K * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
+  return LIK_OK;
+}
+
+int lik_profiles_device(lik_ctx* c, int n, int p, int K, int M, const double* y,
+                        const double* ssqYX, const double* logdetV, const int* status,
+                        const double* lambdas, int G, const double* beta_grid, double* prof_beta,
+                        int Sg, const double* sigma_grid, double* prof_sigma, double* prof_lambda,
+                        void* cuda_stream) {
+  if (!c) return LIK_EINVAL;
+  c->err.clear();
+  if (any_null({y, ssqYX, logdetV, status, lambdas, prof_lambda}) ||
+      (G > 0 && (!beta_grid || !prof_beta)) || (Sg > 0 && (!sigma_grid || !prof_sigma)))
+    return fail(c, LIK_EINVAL, "NULL pointer argument");
+  if (p < 1 || p > 32 || n < p + 2 || K < 1 || M < 1 || G < 0 || Sg < 0)
+    return fail(c, LIK_EINVAL, "bad sizes n=%d p=%d K=%d M=%d G=%d Sg=%d (1 <= p <= 32)", n, p, K, M,
+                G, Sg);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const size_t need = ((size_t)K * p * M * 3 + (size_t)K * M + 2) * sizeof(double);
+  int rc;
+  if ((rc = ensure(c, &c->prof_scratch, &c->prof_scratch_bytes, need))) return rc;
+  double* coefs = c->prof_scratch;
+  double* qfull = coefs + (size_t)K * p * M * 3;
+  double* S = qfull + (size_t)K * M;
+  CUDA_TRY(c, lik::launch_profiles(n, p, K, M, y, ssqYX, logdetV, status, lambdas, G, beta_grid,
+                                   prof_beta, Sg, sigma_grid, prof_sigma, prof_lambda, coefs, qfull,
+                                   S, (cudaStream_t)cuda_stream));
   return LIK_OK;
 }
 

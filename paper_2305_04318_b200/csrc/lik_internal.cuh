@@ -123,6 +123,11 @@ struct CholArgs {
 };
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
 size_t chol_smem_bytes();
+cudaError_t launch_profiles(int n, int p, int K, int M, const double* y, const double* ssqYX,
+                            const double* logdetV, const int* status, const double* lambdas,
+                            int G, const double* beta_grid, double* prof_beta, int Sg,
+                            const double* sigma_grid, double* prof_sigma, double* prof_lambda,
+                            double* coefs, double* qfull, double* S, cudaStream_t st);
 int chol_ctas_per_sm();
 
 }  // namespace lik

@@ -268,3 +268,29 @@ def test_site_order_invariance():
     np.testing.assert_allclose(a["loglik"], b["loglik"], rtol=1e-11)
     np.testing.assert_allclose(a["logdetV"], b["logdetV"], rtol=1e-11, atol=1e-11)
     np.testing.assert_allclose(a["betahat"], b["betahat"], rtol=1e-9, atol=1e-9 * np.abs(a["betahat"]).max())
+
+
+@pytest.mark.parametrize("name,K", [("C1", 16), ("C2", 200)])
+def test_profiles_vs_oracle(ctx, orc, name, K):
+    """NEXT-2: β_a, σ, λ profile log-likelihoods over the K×M grid from the
+    GPU summaries vs the oracle's profiles from its own summaries."""
+    coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
+    n, p = X.shape
+    t = [torch.tensor(a, device="cuda") for a in (coords, y, X, P, lam)]
+    summ = ctx.eval_batch_device_ex(*t)
+    ref = orc.eval_batch(coords, y, X, P, lam, nthreads=NTHREADS, summaries=True)
+    bh = ref["betahat"][ref["status"] == 0].reshape(-1, p)
+    lo, hi = bh.min(axis=0), bh.max(axis=0)
+    span = np.maximum(hi - lo, 1e-3 * np.maximum(1.0, np.abs(bh).max(axis=0)))
+    grid = np.stack([np.linspace(lo[a] - span[a], hi[a] + span[a], 33) for a in range(p)])
+    sig = np.sqrt(np.linspace(0.3, 3.0, 17) * np.median(ref["sigma2hat"]))
+    pb, ps, pl = ctx.profiles_device(n, t[1], summ, t[4], torch.tensor(grid, device="cuda"),
+                                     torch.tensor(sig, device="cuda"))
+    torch.cuda.synchronize()
+    rb, rs, rl = orc.profiles(n, p, ref["ssqYX"], ref["logdetV"], ref["status"], lam, y, grid, sig)
+    rel = lambda a, b: np.abs(a - b) / np.abs(b)
+    assert rel(pb.cpu().numpy(), rb).max() <= 1e-8
+    assert rel(ps.cpu().numpy(), rs).max() <= 1e-8
+    assert rel(pl.cpu().numpy(), rl).max() <= 1e-8
+    # the β profile peaks at the global maximum of ℓ_p over the grid
+    assert pb.cpu().numpy().max() <= ref["loglik"].max() + 1e-9
