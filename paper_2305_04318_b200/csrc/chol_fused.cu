@@ -46,14 +46,17 @@ constexpr int NT = 256;
 // starve behind the co-resident CTA's DMMA warps.
 constexpr int LEAD_WARP = NT / 32 - 1;
 constexpr int LEAD_TID = LEAD_WARP * 32;
-constexpr int NSTAGE = 3;
+#ifndef LIK_NSTAGE
+#define LIK_NSTAGE 3
+#endif
+constexpr int NSTAGE = LIK_NSTAGE;  // stage ring depth (3 fits two CTAs per SM)
 constexpr int STAGE_D = 3 * CHUNK_D;             // A rows of tile a, A rows of tile b, B rows
 constexpr int OFF_SCRATCH = 2 * TILE_D;          // 32×32 scratch after the staging tiles
 constexpr int OFF_LINV = NSTAGE * STAGE_D;
 constexpr int OFF_DLOG = OFF_LINV + TILE_D;
 constexpr int OFF_MISC = OFF_DLOG + 64;          // 8 doubles of scalars
-constexpr int OFF_MBAR = OFF_MISC + 8;           // NSTAGE uint64
-constexpr int SMEM_D = OFF_MBAR + NSTAGE + 4;    // + int flags[4], cnt[NSTAGE]
+constexpr int OFF_MBAR = OFF_MISC + 8;           // NSTAGE full + NSTAGE empty uint64
+constexpr int SMEM_D = OFF_MBAR + 2 * NSTAGE + 4;  // + int flags[4]
 static_assert(OFF_SCRATCH + 32 * 32 <= OFF_LINV, "staging + scratch must fit in the stage ring");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -72,6 +75,9 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
@@ -235,6 +241,46 @@ __device__ __forceinline__ void frag_sub_from(Acc& acc, const double* __restrict
     }
 }
 
+// acc −= T (T split: rows < off from T1, rows ≥ off from T2 at row − off)
+__device__ __forceinline__ void frag_sub_from2(Acc& acc, const double* __restrict__ T1,
+                                               const double* __restrict__ T2, int off, int rbase,
+                                               int cbase, int mlim, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+    if (mi < mlim) {
+      const int row = rbase + mi * 8 + lr;
+      const double* T = row < off ? T1 : T2;
+      const int rr = row < off ? row : row - off;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const double2 v = *reinterpret_cast<const double2*>(T + sw_off(rr, cbase + ni * 8 + 2 * lc));
+        acc[mi][ni][0] -= v.x;
+        acc[mi][ni][1] -= v.y;
+      }
+    }
+}
+
+__device__ __forceinline__ void frag_store2(const Acc& acc, double* __restrict__ T1,
+                                            double* __restrict__ T2, int off, int rbase,
+                                            int cbase, int mlim, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+    if (mi < mlim) {
+      const int row = rbase + mi * 8 + lr;
+      double* T = row < off ? T1 : T2;
+      const int rr = row < off ? row : row - off;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        double2 v;
+        v.x = acc[mi][ni][0];
+        v.y = acc[mi][ni][1];
+        *reinterpret_cast<double2*>(T + sw_off(rr, cbase + ni * 8 + 2 * lc)) = v;
+      }
+    }
+}
+
 template <bool NEG>
 __device__ __forceinline__ void frag_store(const Acc& acc, double* __restrict__ T, int rbase,
                                            int cbase, int mlim, int lane) {
@@ -262,49 +308,67 @@ __device__ __forceinline__ void frag_zero(Acc& acc) {
 struct Pipe {
   double* stages;
   uint64_t* mbar;     // "full" barriers: complete when a stage's bulk copies landed
-  int* cnt;           // per-stage count of warps done reading it
+  uint64_t* empty;    // "empty" barriers: complete when all 8 warps finished reading a stage
   uint32_t seq;       // chunks consumed so far (same value in every thread)
   uint64_t pol_stream, pol_keep;
+};
+
+// A k-loop operand: rows [0, r1) of row panel p1 and, for a merged tail tile,
+// rows [0, r2) of row panel p2 placed at buffer row r1 (r1 a multiple of 16, so the
+// chunk swizzle, which depends on row & 3, is preserved).
+struct Src {
+  const double* p1;
+  int r1;
+  const double* p2;
+  int r2;
 };
 
 // acc += Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
 //   A rows of tile a: gA0 + q·CHUNK_D (cA0 rows copied), tile b: gA1 (cA1 rows),
 //   B rows: gB (cB rows).
 // There is no CTA-wide barrier per chunk: each warp waits only for its data
-// (mbarrier), and the last of the 8 warps to finish reading a stage (counted
-// with a shared-memory atomic) refills it with the chunk NSTAGE ahead.  The
-// caller must __syncthreads() between two k-loops.
-__device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, const double* gA0, int cA0,
-                                      const double* gA1, int cA1, const double* gB, int cB,
-                                      int nq, bool mine_b, int rbase, int mlim, int cbase,
-                                      int lane) {
+// (full mbarrier) and releases the stage with a non-blocking arrive on its empty
+// mbarrier; the lead warp, at the start of chunk q, waits for the stage of chunk
+// q−1 to be released and refills it with chunk q−1+NSTAGE.  The caller must
+// __syncthreads() between two k-loops.
+__device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
+                                      bool mine_b, int rbase, int mlim, int cbase, int lane) {
   const int tid = threadIdx.x;
   const uint32_t seq = pp.seq;
+  auto copy = [&](double* dst, const Src& sr, int q, uint32_t bar, uint64_t pol) {
+    if (sr.r1) bulk_g2s(saddr(dst), sr.p1 + (size_t)q * CHUNK_D, sr.r1 * KC * 8, bar, pol);
+    if (sr.r2)
+      bulk_g2s(saddr(dst + sr.r1 * KC), sr.p2 + (size_t)q * CHUNK_D, sr.r2 * KC * 8, bar, pol);
+  };
   auto issue = [&](int q) {
     const uint32_t s = (seq + q) % NSTAGE;
     double* st = pp.stages + s * STAGE_D;
     const uint32_t bar = saddr(&pp.mbar[s]);
-    mbar_expect_tx(bar, (uint32_t)(cA0 + cA1 + cB) * KC * 8);
-    bulk_g2s(saddr(st), gA0 + (size_t)q * CHUNK_D, cA0 * KC * 8, bar, pp.pol_stream);
-    if (cA1)
-      bulk_g2s(saddr(st + CHUNK_D), gA1 + (size_t)q * CHUNK_D, cA1 * KC * 8, bar, pp.pol_stream);
-    bulk_g2s(saddr(st + 2 * CHUNK_D), gB + (size_t)q * CHUNK_D, cB * KC * 8, bar, pp.pol_keep);
+    mbar_expect_tx(bar, (uint32_t)(A0.r1 + A0.r2 + A1.r1 + A1.r2 + B.r1 + B.r2) * KC * 8);
+    copy(st, A0, q, bar, pp.pol_stream);
+    copy(st + CHUNK_D, A1, q, bar, pp.pol_stream);
+    copy(st + 2 * CHUNK_D, B, q, bar, pp.pol_keep);
   };
   if (tid == LEAD_TID)
     for (int q = 0; q < NSTAGE && q < nq; ++q) issue(q);
   for (int q = 0; q < nq; ++q) {
+    if (tid == LEAD_TID && q >= 1 && q - 1 + NSTAGE < nq) {
+      const uint32_t u = seq + q - 1;
+      mbar_wait(saddr(&pp.empty[u % NSTAGE]), (u / NSTAGE) & 1);
+      issue(q - 1 + NSTAGE);
+    }
     const uint32_t s = (seq + q) % NSTAGE;
+#ifdef LIK_PHASE_TIMERS
+    const long long tw0 = clock64();
+#endif
     mbar_wait(saddr(&pp.mbar[s]), ((seq + q) / NSTAGE) & 1);
+#ifdef LIK_PHASE_TIMERS
+    if (tid == 224) atomicAdd(&g_lik_phase[q == 0 ? 9 : 15], (unsigned long long)(clock64() - tw0));
+#endif
     const double* st = pp.stages + s * STAGE_D;
     mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, cbase, lane);
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();  // this warp's reads of stage s precede the arrival
-      if (atomicAdd(&pp.cnt[s], 1) == NT / 32 - 1) {
-        pp.cnt[s] = 0;
-        if (q + NSTAGE < nq) issue(q + NSTAGE);
-      }
-    }
+    if (lane == 0) mbar_arrive(saddr(&pp.empty[s]));
   }
   pp.seq = seq + nq;
 }
@@ -477,6 +541,106 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
   return 0;
 }
 
+// Partial Cholesky of the merged last diagonal tile: pivots are the first v
+// (= vlast) columns; the augmented rows start at row `off` (a multiple of 16 ≥ v).
+// Panels of 16 as in potrf_inv64 (factor + invert the pivot block in registers,
+// panel product, trailing update), stopping after the last pivot panel: the
+// block rows/cols ≥ off then hold C_BB − Z Zᵀ = −BᵀV⁻¹B (the Schur complement).
+__device__ int potrf_tail(double* S, int v, double tol, double* dlog, int* flag, double* X) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c0 = 0; c0 < v; c0 += 16) {
+    const int vloc = min(16, v - c0);
+    if (warp == LEAD_WARP) {
+      const int l = lane & 15;
+      double a[16];
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) a[kk] = (kk <= l) ? S[sw_off(c0 + l, c0 + kk)] : 0.0;
+      int bad = 0;
+      double my_piv = 1.0, my_rinv = 1.0;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (c < vloc) {
+          const double piv = __shfl_sync(0xffffffffu, a[c], c);
+          bad |= !(piv > tol);
+          const double rinv = rsqrt(piv);
+          if (l == c) {
+            a[c] = piv * rinv;
+            my_piv = piv;
+            my_rinv = rinv;
+          } else if (l > c) {
+            a[c] *= rinv;
+          }
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) {
+            if (kk > c) {
+              const double lk = __shfl_sync(0xffffffffu, a[c], kk);
+              if (l >= kk) a[kk] -= a[c] * lk;
+            }
+          }
+        }
+      }
+      if (lane < 16 && l < vloc) dlog[c0 + l] = log(my_piv);
+      double x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = (i == l && l < vloc) ? 1.0 : 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < vloc) {
+          x[i] *= __shfl_sync(0xffffffffu, my_rinv, i);
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk)
+            if (kk > i) x[kk] -= __shfl_sync(0xffffffffu, a[i], kk) * x[i];
+        }
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          if (kk <= l) S[sw_off(c0 + l, c0 + kk)] = a[kk];
+          X[sw_off(c0 + kk, c0 + l)] = (kk < vloc && l < vloc) ? x[kk] : 0.0;
+        }
+      }
+      if (lane == 0 && bad) flag[0] = 1;
+    }
+    __syncthreads();
+    if (flag[0]) return 1;
+    if (c0 + 16 < TB) {
+      const int base = c0 + 16, m = TB - base;
+      double xv[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int e = tid + q * NT;
+        xv[q] = 0.0;
+        if (e < m * 16) {
+          const int i = base + (e >> 4), c = e & 15;
+          double acc1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk)
+            if (kk <= c) acc1 += S[sw_off(i, c0 + kk)] * X[sw_off(c0 + c, c0 + kk)];
+          xv[q] = acc1;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int e = tid + q * NT;
+        if (e < m * 16) S[sw_off(base + (e >> 4), c0 + (e & 15))] = xv[q];
+      }
+      __syncthreads();
+      for (int e = tid; e < m * m; e += NT) {
+        const int i = base + e / m, kk = base + e % m;
+        if (kk <= i) {
+          double acc1 = S[sw_off(i, kk)];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) acc1 -= S[sw_off(i, c0 + c)] * S[sw_off(kk, c0 + c)];
+          S[sw_off(i, kk)] = acc1;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  return 0;
+}
+
 __device__ void write_point_failure(const CholArgs& A, int k, int code) {
   const int tid = threadIdx.x;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
@@ -507,8 +671,8 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   double* dlog = sm + OFF_DLOG;
   double* scal = sm + OFF_MISC;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + OFF_MBAR);
-  int* flag = reinterpret_cast<int*>(sm + OFF_MBAR + NSTAGE);
-  int* cnt = flag + 4;
+  uint64_t* mbar_empty = mbar + NSTAGE;
+  int* flag = reinterpret_cast<int*>(sm + OFF_MBAR + 2 * NSTAGE);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w >> 1, wc = w & 1;
@@ -527,25 +691,34 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   }
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) mbar_init(saddr(&mbar[s]), 1);
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(saddr(&mbar_empty[s]), NT / 32);
     flag[0] = flag[1] = flag[2] = 0;
-    for (int s = 0; s < NSTAGE; ++s) cnt[s] = 0;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   __syncthreads();
 
-  Pipe pp{sm, mbar, cnt, 0u, policy_evict_first(), policy_evict_last()};
+  Pipe pp{sm, mbar, mbar_empty, 0u, policy_evict_first(), policy_evict_last()};
   const double tol = g.n * DBL_EPSILON * (1.0 + nugget);
   double logdet = 0.0;  // meaningful in thread 0
-  auto valid_rows = [&](int ti) { return ti == nt ? g.Ra : (ti == nt - 1 ? g.vlast : TB); };
+  const bool MG = g.merged;  // merged tail (see SlotGeom): tile row nt−1 also carries the B rows
+  auto is_m = [&](int ti) { return MG && ti == nt - 1; };
+  auto valid_rows = [&](int ti) {
+    return ti == nt ? g.Ra : (is_m(ti) ? g.off + g.Ra : (ti == nt - 1 ? g.vlast : TB));
+  };
   auto copy_rows = [&](int ti) { return ti == nt ? g.Ra : TB; };
   auto tile_ptr = [&](int ti, int tj) -> double* {
     return ws + (size_t)(ti == nt ? g.ntri + tj : tri_index(ti, tj)) * TILE_D;
+  };
+  auto src = [&](int ti) -> Src {  // k-loop operand: the row panel of tile row ti
+    if (ti < 0) return Src{nullptr, 0, nullptr, 0};
+    if (is_m(ti)) return Src{tile_ptr(ti, 0), g.off, tile_ptr(nt, 0), g.Ra};
+    return Src{tile_ptr(ti, 0), copy_rows(ti), nullptr, 0};
   };
 
   Acc acc;
   PH_INIT();
   for (int j = 0; j < nt; ++j) {
-    const int nrow = nt - j + 1;  // tile rows j..nt-1 and the augmented row
+    const int nrow = MG ? nt - j : nt - j + 1;  // tile rows j..nt-1 (and the augmented row)
     for (int rb = 0; rb < nrow; rb += 2) {
       const int ia = j + rb;
       const int ib = (rb + 1 < nrow) ? j + rb + 1 : -1;
@@ -561,18 +734,32 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
       // acc = Σ_k L_ik L_jkᵀ, then C = A_ij − acc (stored negated in the staging below)
       frag_zero(acc);
       PH(0);
-      if (j > 0)
-        kloop(acc, pp, tile_ptr(ia, 0), copy_rows(ia), ib >= 0 ? tile_ptr(ib, 0) : nullptr,
-              ib >= 0 ? copy_rows(ib) : 0, tile_ptr(j, 0), TB, CHUNKS * j, mine_b, rbase, mlim,
-              cbase, lane);
+      if (j > 0) kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, cbase, lane);
       PH(1);
-      frag_sub_from(acc, tile_ptr(mine_b ? (ib >= 0 ? ib : ia) : ia, j), rbase, cbase, mlim, lane);
+      {
+        const int ti = mine_b ? (ib >= 0 ? ib : ia) : ia;
+        if (is_m(ti))
+          frag_sub_from2(acc, tile_ptr(ti, j), tile_ptr(nt, j), g.off, rbase, cbase, mlim, lane);
+        else
+          frag_sub_from(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
+      }
       __syncthreads();
       PH(2);
       frag_store<true>(acc, staging + (mine_b ? TILE_D : 0), rbase, cbase, mlim, lane);
       __syncthreads();
       PH(3);
-      if (rb == 0) {
+      if (rb == 0 && is_m(j)) {
+        // merged last diagonal tile: partial factorisation; its Schur block is −BᵀV⁻¹B
+        if (potrf_tail(staging, g.vlast, tol, dlog, flag, Linv)) {
+          write_point_failure(A, k, LIK_PT_V_NOT_PD);
+          return;
+        }
+        if (tid == LEAD_TID) {
+          double s = 0.0;
+          for (int c = 0; c < g.vlast; ++c) s += dlog[c];
+          logdet += s;
+        }
+      } else if (rb == 0) {
         // diagonal tile: factor, log-determinant, inverse for this column's solves
         if (potrf_inv64(staging, valid_rows(j), tol, dlog, flag, Linv, sm + OFF_SCRATCH)) {
           write_point_failure(A, k, LIK_PT_V_NOT_PD);
@@ -589,14 +776,20 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
         if (ib >= 0 && mine_b) {
           frag_zero(acc);
           trsm_any(acc, staging + TILE_D, rbase, mlim, Linv, wc, lane);
-          frag_store<false>(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
+          if (is_m(ib))
+            frag_store2(acc, tile_ptr(ib, j), tile_ptr(nt, j), g.off, rbase, cbase, mlim, lane);
+          else
+            frag_store<false>(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
         }
       } else {
         // L_ij = C L_jj⁻ᵀ for both tile rows of the block
         frag_zero(acc);
         trsm_any(acc, staging + (mine_b ? TILE_D : 0), rbase, mlim, Linv, wc, lane);
         const int ti = mine_b ? ib : ia;
-        if (ti >= 0) frag_store<false>(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
+        if (ti >= 0 && is_m(ti))
+          frag_store2(acc, tile_ptr(ti, j), tile_ptr(nt, j), g.off, rbase, cbase, mlim, lane);
+        else if (ti >= 0)
+          frag_store<false>(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
       }
       PH(6);
       // L tiles written in column j are read through TMA only from column j+1 on
@@ -607,12 +800,13 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
     }
   }
 
-  // Final block of the augmented row: acc = Σ_k Z_k Z_kᵀ = BᵀV⁻¹B  (ssqYX, Table 1)
-  {
+  // ssqYX = BᵀV⁻¹B (Table 1, Step 4)
+  if (!MG) {
+    // separate augmented row: acc = Σ_k Z_k Z_kᵀ over its final block
     const int mlim = mine_b ? 0 : max(0, min(4, (g.Ra - rbase + 7) >> 3));
     frag_zero(acc);
-    kloop(acc, pp, tile_ptr(nt, 0), g.Ra, nullptr, 0, tile_ptr(nt, 0), g.Ra, CHUNKS * nt, false,
-          rbase, mlim, cbase, lane);
+    kloop(acc, pp, src(nt), Src{nullptr, 0, nullptr, 0}, src(nt), CHUNKS * nt, false, rbase, mlim,
+          cbase, lane);
     __syncthreads();
     frag_store<false>(acc, staging, rbase, cbase, mlim, lane);
     __syncthreads();
@@ -622,7 +816,8 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   double* Q = staging + TILE_D;  // p×p Cholesky factor of XᵀV⁻¹X (stride 64)
   for (int e = tid; e < r * r; e += NT) {
     const int a = e / r, b = e % r;
-    Cm[a * 64 + b] = staging[sw_off(a, b)];
+    // merged: the Schur block (lower triangle) of the last diagonal tile is −BᵀV⁻¹B
+    Cm[a * 64 + b] = MG ? -staging[sw_off(g.off + max(a, b), g.off + min(a, b))] : staging[sw_off(a, b)];
   }
   __syncthreads();
   if (A.ssqYX)

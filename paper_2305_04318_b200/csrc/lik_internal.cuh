@@ -44,6 +44,13 @@ struct SlotGeom {
   int r;       // M + p (augmented rows)
   int Ra;      // r rounded up to a multiple of 8 (rows copied / computed)
   size_t slot_d;  // doubles per slot = (ntri + nt) * TILE_D
+  // Merged tail: when the last V tile is ragged and its padding can hold the r
+  // augmented rows (off + Ra ≤ 64, off = vlast rounded up to 16), the B rows are
+  // treated as rows off.. of the last tile row (a virtual tile assembled from two
+  // bulk copies), so no separate augmented tile row is processed and the last
+  // diagonal tile's partial factorisation leaves −BᵀV⁻¹B as its Schur block.
+  int merged;
+  int off;
 };
 
 inline SlotGeom make_geom(int n, int r) {
@@ -55,6 +62,8 @@ inline SlotGeom make_geom(int n, int r) {
   g.r = r;
   g.Ra = (r + 7) & ~7;
   g.slot_d = (size_t)(g.ntri + g.nt) * TILE_D;
+  g.off = (g.vlast + 15) & ~15;
+  g.merged = (r > 0 && g.vlast < TB && g.off + g.Ra <= TB) ? 1 : 0;
   return g;
 }
 
