@@ -53,7 +53,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 
 
 if __name__ == "__main__":
-    if "--phase-timers" in sys.argv:
+    if "--bounds-check" in sys.argv:
+        print(build(force=True, defines=("LIK_BOUNDS_CHECK",), out=os.path.join(HERE, "liblik_bounds.so")))
+    elif "--phase-timers" in sys.argv:
         extra = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
         print(build(force=True, defines=("LIK_PHASE_TIMERS",) + extra, out=os.path.join(HERE, "liblik_phase.so")))
     else:

@@ -23,6 +23,7 @@
 // point (diagonal factorisation, inverse) overlap the DMMA phases of the other.
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
 #include "../../include/lik.h"
 #include "lik_internal.cuh"
 
@@ -323,6 +324,21 @@ struct Src {
   int r2;
 };
 
+#ifdef LIK_BOUNDS_CHECK
+// Debug builds: every bulk-copy source range and tile pointer must lie inside the
+// point's workspace slot [lo, hi) (compute-sanitizer is unavailable on the pool).
+#define LIK_CHECK_RANGE(ptr, ndoubles, lo, hi)                                              \
+  do {                                                                                      \
+    if ((const double*)(ptr) < (lo) || (const double*)(ptr) + (ndoubles) > (hi)) {          \
+      printf("lik bounds: block %d ptr %p + %ld outside [%p, %p)\n", blockIdx.x, (const void*)(ptr), \
+             (long)(ndoubles), (const void*)(lo), (const void*)(hi));                       \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define LIK_CHECK_RANGE(ptr, ndoubles, lo, hi) do {} while (0)
+#endif
+
 // acc += Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
 //   A rows of tile a: gA0 + q·CHUNK_D (cA0 rows copied), tile b: gA1 (cA1 rows),
 //   B rows: gB (cB rows).
@@ -332,10 +348,13 @@ struct Src {
 // q−1 to be released and refills it with chunk q−1+NSTAGE.  The caller must
 // __syncthreads() between two k-loops.
 __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
-                                      bool mine_b, int rbase, int mlim, int cbase, int lane) {
+                                      bool mine_b, int rbase, int mlim, int cbase, int lane,
+                                      const double* slot_lo, const double* slot_hi) {
   const int tid = threadIdx.x;
   const uint32_t seq = pp.seq;
   auto copy = [&](double* dst, const Src& sr, int q, uint32_t bar, uint64_t pol) {
+    if (sr.r1) LIK_CHECK_RANGE(sr.p1 + (size_t)q * CHUNK_D, sr.r1 * KC, slot_lo, slot_hi);
+    if (sr.r2) LIK_CHECK_RANGE(sr.p2 + (size_t)q * CHUNK_D, sr.r2 * KC, slot_lo, slot_hi);
     if (sr.r1) bulk_g2s(saddr(dst), sr.p1 + (size_t)q * CHUNK_D, sr.r1 * KC * 8, bar, pol);
     if (sr.r2)
       bulk_g2s(saddr(dst + sr.r1 * KC), sr.p2 + (size_t)q * CHUNK_D, sr.r2 * KC * 8, bar, pol);
@@ -707,7 +726,9 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
   };
   auto copy_rows = [&](int ti) { return ti == nt ? g.Ra : TB; };
   auto tile_ptr = [&](int ti, int tj) -> double* {
-    return ws + (size_t)(ti == nt ? g.ntri + tj : tri_index(ti, tj)) * TILE_D;
+    double* t = ws + (size_t)(ti == nt ? g.ntri + tj : tri_index(ti, tj)) * TILE_D;
+    LIK_CHECK_RANGE(t, TILE_D, ws, ws + g.slot_d);
+    return t;
   };
   auto src = [&](int ti) -> Src {  // k-loop operand: the row panel of tile row ti
     if (ti < 0) return Src{nullptr, 0, nullptr, 0};
@@ -734,7 +755,9 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
       // acc = Σ_k L_ik L_jkᵀ, then C = A_ij − acc (stored negated in the staging below)
       frag_zero(acc);
       PH(0);
-      if (j > 0) kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, cbase, lane);
+      if (j > 0)
+        kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, cbase, lane, ws,
+              ws + g.slot_d);
       PH(1);
       {
         const int ti = mine_b ? (ib >= 0 ? ib : ia) : ia;
@@ -806,7 +829,7 @@ __global__ void __launch_bounds__(NT, 2) chol_fused_kernel(CholArgs A) {
     const int mlim = mine_b ? 0 : max(0, min(4, (g.Ra - rbase + 7) >> 3));
     frag_zero(acc);
     kloop(acc, pp, src(nt), Src{nullptr, 0, nullptr, 0}, src(nt), CHUNKS * nt, false, rbase, mlim,
-          cbase, lane);
+          cbase, lane, ws, ws + g.slot_d);
     __syncthreads();
     frag_store<false>(acc, staging, rbase, cbase, mlim, lane);
     __syncthreads();

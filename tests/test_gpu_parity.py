@@ -294,3 +294,22 @@ def test_profiles_vs_oracle(ctx, orc, name, K):
     assert rel(pl.cpu().numpy(), rl).max() <= 1e-8
     # the β profile peaks at the global maximum of ℓ_p over the grid
     assert pb.cpu().numpy().max() <= ref["loglik"].max() + 1e-9
+
+
+def test_bounds_checked_build():
+    """The LIK_BOUNDS_CHECK build traps if any bulk copy or tile pointer leaves the point's
+    workspace slot; run the sanitizer case (C1, ragged C2, merged and separate augmented
+    tails, profiles, debug V) in a subprocess with it (compute-sanitizer is closed on
+    the pool)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_b = os.path.join(root, "paper_2305_04318_b200", "liblik_bounds.so")
+    if not os.path.exists(lib_b):
+        from paper_2305_04318_b200 import build as b
+        b.build(force=True, defines=("LIK_BOUNDS_CHECK",), out=lib_b)
+    env = dict(os.environ, LIK_LIBRARY=lib_b)
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "debug", "sanitize_case.py")], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "lik bounds" not in r.stdout + r.stderr
