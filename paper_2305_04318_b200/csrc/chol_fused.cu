@@ -206,25 +206,6 @@ __device__ __forceinline__ void trsm_any(Acc& acc, const double* Sb, int rbase, 
   }
 }
 
-__device__ __forceinline__ void frag_load_neg(Acc& acc, const double* __restrict__ T, int rbase,
-                                              int cbase, int mlim, int lane) {
-  const int lr = lane >> 2, lc = lane & 3;
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      if (mi < mlim) {
-        const double2 v = *reinterpret_cast<const double2*>(
-            T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc));
-        acc[mi][ni][0] = -v.x;
-        acc[mi][ni][1] = -v.y;
-      } else {
-        acc[mi][ni][0] = 0.0;
-        acc[mi][ni][1] = 0.0;
-      }
-    }
-}
-
 // acc = acc − T  (T = the A_ij tile in global memory), i.e. −C.
 __device__ __forceinline__ void frag_sub_from(Acc& acc, const double* __restrict__ T, int rbase,
                                               int cbase, int mlim, int lane) {
