@@ -48,7 +48,7 @@ constexpr int NT = 256;
 constexpr int LEAD_WARP = NT / 32 - 1;
 constexpr int LEAD_TID = LEAD_WARP * 32;
 #ifndef LIK_NSTAGE
-#define LIK_NSTAGE 3
+#define LIK_NSTAGE (KC == 8 ? 6 : 3)
 #endif
 constexpr int NSTAGE = LIK_NSTAGE;  // stage ring depth (3 fits two CTAs per SM)
 constexpr int STAGE_D = 3 * CHUNK_D;             // A rows of tile a, A rows of tile b, B rows
@@ -125,7 +125,7 @@ template <bool MFULL>
 __device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ Ab, int rbase,
                                           int mlim, const double* __restrict__ Bb, int cbase,
                                           int lane) {
-  const int lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
+  const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
 #pragma unroll
   for (int kk = 0; kk < KC / 4; ++kk) {
     const int kcol = ((kk * 4) ^ sw) + lc;
@@ -165,7 +165,7 @@ __device__ __forceinline__ void mma_chunk_any(Acc& acc, const double* Ab, int rb
 template <int WC, bool MFULL>
 __device__ __forceinline__ void trsm_tri(Acc& acc, const double* __restrict__ Sb, int rbase,
                                          int mlim, const double* __restrict__ X, int lane) {
-  const int lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
+  const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
   constexpr int cb = WC * 32;
 #pragma unroll
   for (int h = 0; h < CHUNKS; ++h) {

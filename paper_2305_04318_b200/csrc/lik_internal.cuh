@@ -26,13 +26,23 @@ namespace lik {
 // 4j chunks.
 // ---------------------------------------------------------------------------
 constexpr int TB = 64;              // tile edge
-constexpr int KC = 16;              // chunk width (k-extent of one pipeline stage)
+#ifndef LIK_KC
+#define LIK_KC 16
+#endif
+constexpr int KC = LIK_KC;          // chunk width (k-extent of one pipeline stage): 8 or 16
 constexpr int CHUNKS = TB / KC;     // chunks per tile
 constexpr int TILE_D = TB * TB;     // doubles per tile
 constexpr int CHUNK_D = TB * KC;    // doubles per chunk
+static_assert(KC == 8 || KC == 16, "chunk width");
 
+// XOR swizzle of the column within a chunk row: the 16 lanes of a half-warp read
+// rows r0..r0+3 × columns 4q..4q+3 of a DMMA fragment; the swizzle spreads them over
+// 16 distinct 8-byte bank slots (KC = 16: rows differ by 16 doubles; KC = 8: by 8).
+__host__ __device__ __forceinline__ int swz(int row) {
+  return KC == 16 ? ((row & 3) << 2) : (((row >> 1) & 1) << 2);
+}
 __host__ __device__ __forceinline__ int sw_off(int row, int col) {
-  return ((col >> 4) << 10) + (row << 4) + ((col & 15) ^ ((row & 3) << 2));
+  return (col / KC) * CHUNK_D + row * KC + ((col % KC) ^ swz(row));
 }
 __host__ __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
