@@ -8,6 +8,7 @@ import json, math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synthgen, paper_2305_04318_b200 as lik
+from paper_2305_04318_b200 import representative as rp
 
 
 def workload(name, n, p, K, M, seed):
@@ -47,8 +48,19 @@ for name, n, p, K, M in (("swiss", 100, 2, 15318, 34), ("soil", 829, 18, 12316, 
     ev_ms, pr_ms = e[0].elapsed_time(e[1]) / reps, e[1].elapsed_time(e[2]) / reps
     r = M + p
     F = n ** 3 / 3 + n * n * r + n * r * r
+    # Step 2: 6 fits (κ free + the 5 κ-fixed of P:582), stencil Hessians on the
+    # GPU (51·3 / 33·3 likelihoods each), 726 / 120 sphere points × 12 α, λ grid of M−1 + λ̂
+    nat = np.array(P[0]); nat[1] = 2.0
+    fits = [rp.Fit(nat, 0.5)] + [rp.Fit(np.r_[nat[0], kf, nat[2:]], 0.5, kappa_fixed=kf)
+                                 for kf in synthgen.KAPPA_FIXED]
+    import time
+    t0 = time.perf_counter(); rs = rp.configure_params(ctx, coords, y, X, fits, m_lambda=M - 1)
+    t1 = time.perf_counter(); rs = rp.configure_params(ctx, coords, y, X, fits, m_lambda=M - 1)
+    t2 = time.perf_counter()
     print(json.dumps({"workload": name, "n": n, "p": p, "K": K, "M": M,
                       "eval_ms": round(ev_ms, 3), "points_per_s": K / (ev_ms / 1e3),
                       "likelihoods_per_s": K * M / (ev_ms / 1e3), "dense_fp64_tflops": K * F / (ev_ms / 1e3) / 1e12,
-                      "profiles_ms": round(pr_ms, 3), "status_ok": int(ok.sum()),
+                      "profiles_ms": round(pr_ms, 3),
+                      "step2_ms_cold": round((t1 - t0) * 1e3, 1), "step2_ms_warm": round((t2 - t1) * 1e3, 1),
+                      "step2_points": int(len(rs.params)), "step2_lambdas": int(len(rs.lambdas)), "status_ok": int(ok.sum()),
                       "stages_ms": {k: round(v[0] / reps, 3) for k, v in ctx.stage_times().items()}}), flush=True)
