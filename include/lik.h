@@ -161,8 +161,11 @@ int lik_profiles_device(lik_ctx* ctx, int n, int p, int K, int M, const double* 
 int lik_get_stage_times(lik_ctx* ctx, double* ms, long long* launches);
 int lik_reset_stage_times(lik_ctx* ctx);
 
-/* Points processed concurrently per wave (0 = automatic: one per SM slot,
- * bounded by free HBM).  Results do not depend on it (determinism tests). */
+/* Points per wave, i.e. per build/factor launch (0 = automatic: the fewest
+ * balanced waves of at most 16 × (2 × #SMs) points within half the free HBM;
+ * an explicit value is capped at 85 % of free HBM).  The workspace holds one
+ * slot per wave point (C4: 17.9 MB).  Results do not depend on it
+ * (determinism tests). */
 int lik_set_wave_points(lik_ctx* ctx, int points_per_wave);
 
 /* Debug / parity entry: the dense V = R + ν²I (n×n full, row-major) for each

@@ -55,6 +55,11 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 if __name__ == "__main__":
     if "--bounds-check" in sys.argv:
         print(build(force=True, defines=("LIK_BOUNDS_CHECK",), out=os.path.join(HERE, "liblik_bounds.so")))
+    elif "--variant" in sys.argv:
+        # A/B builds: --variant NAME -DX -DY  ->  liblik_NAME.so
+        name = sys.argv[sys.argv.index("--variant") + 1]
+        extra = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
+        print(build(force=True, defines=extra, out=os.path.join(HERE, f"liblik_{name}.so")))
     elif "--phase-timers" in sys.argv:
         extra = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
         print(build(force=True, defines=("LIK_PHASE_TIMERS",) + extra, out=os.path.join(HERE, "liblik_phase.so")))

@@ -351,6 +351,66 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
   };
   if (tid == LEAD_TID)
     for (int q = 0; q < NSTAGE && q < nq; ++q) issue(q);
+#ifndef LIK_NO_SWP
+  if (mlim == 4) {
+    // Software-pipelined full-tile path: the fragments of k-step t+1 (and, at a
+    // chunk's last k-step, the first fragments of the next chunk, after waiting on
+    // its full barrier) are loaded before the 16 DMMAs of k-step t are issued, so
+    // the shared-memory latency is off the DMMA issue chain.
+    const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
+    const int aoff = mine_b ? CHUNK_D : 0;
+    double fa[2][4], fb[2][4];
+    auto stage_of = [&](int q) { return pp.stages + ((seq + q) % NSTAGE) * STAGE_D; };
+    auto wait_full = [&](int q) {
+      const uint32_t u = seq + q;
+      mbar_wait(saddr(&pp.mbar[u % NSTAGE]), (u / NSTAGE) & 1);
+    };
+    auto load = [&](double (&a)[4], double (&b)[4], const double* st, int kk) {
+      const int kcol = ((kk * 4) ^ sw) + lc;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = st[aoff + (rbase + mi * 8 + lr) * KC + kcol];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = st[2 * CHUNK_D + (cbase + ni * 8 + lr) * KC + kcol];
+    };
+    wait_full(0);
+    load(fa[0], fb[0], stage_of(0), 0);
+    for (int q = 0; q < nq; ++q) {
+      if (tid == LEAD_TID && q >= 1 && q - 1 + NSTAGE < nq) {
+        const uint32_t u = seq + q - 1;
+        mbar_wait(saddr(&pp.empty[u % NSTAGE]), (u / NSTAGE) & 1);
+        issue(q - 1 + NSTAGE);
+      }
+      const double* st = stage_of(q);
+#pragma unroll
+      for (int kk = 0; kk < KC / 4; ++kk) {
+        const int cur = kk & 1;  // KC/4 is even: chunk q+1 starts again in buffer 0
+        if (kk + 1 < KC / 4) {
+          load(fa[cur ^ 1], fb[cur ^ 1], st, kk + 1);
+        }
+#ifdef LIK_SWP_CROSS
+        else if (q + 1 < nq) {
+          wait_full(q + 1);
+          load(fa[cur ^ 1], fb[cur ^ 1], stage_of(q + 1), 0);
+        }
+#endif
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], fa[cur][mi], fb[cur][ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(saddr(&pp.empty[(seq + q) % NSTAGE]));
+#ifndef LIK_SWP_CROSS
+      if (q + 1 < nq) {
+        wait_full(q + 1);
+        load(fa[0], fb[0], stage_of(q + 1), 0);
+      }
+#endif
+    }
+    pp.seq = seq + nq;
+    return;
+  }
+#endif
   for (int q = 0; q < nq; ++q) {
     if (tid == LEAD_TID && q >= 1 && q - 1 + NSTAGE < nq) {
       const uint32_t u = seq + q - 1;

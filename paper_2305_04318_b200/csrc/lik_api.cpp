@@ -2,7 +2,9 @@
 // kernel launches and stage timing.  Host code only; every arithmetic step of
 // the likelihood runs in the CUDA kernels (matern_build.cu, chol_fused.cu).
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -169,6 +171,19 @@ void morton_order(int n, const double* coords, std::vector<int>& perm) {
   for (int i = 0; i < n; ++i) perm[i] = key[i].second;
 }
 
+// LIK_HOST_TRACE=1: per-section wall times of the host side of a call (stderr).
+struct HostTrace {
+  bool on = std::getenv("LIK_HOST_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto u = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[lik host] %-22s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(u - t).count());
+    t = u;
+  }
+};
+
 cudaEvent_t ev_get(lik_ctx* c, size_t i) {
   while (c->ev.size() <= i) {
     cudaEvent_t e;
@@ -188,18 +203,31 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
                int K, const double* params, int M, const double* lambdas, double* loglik,
                double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st,
                const double* hcoords, const Extras& ex = Extras()) {
+  HostTrace tr;
   const SlotGeom g = lik::make_geom(n, M + p);
   const size_t slot_bytes = g.slot_d * sizeof(double);
-  int W = c->wave_points > 0 ? c->wave_points : c->nsm * lik::chol_ctas_per_sm();
-  W = std::min(W, K);
+  // Wave size W (points per table/build/chol launch).  All CTAs of a chol launch
+  // start together and the launch ends with its slowest point, so fewer, larger
+  // launches lose less to that tail (the CTA scheduler backfills within a launch):
+  // by default the fewest balanced waves of at most 16 × (resident CTAs per GPU)
+  // points that fit in half the free HBM.  lik_set_wave_points overrides (85 % cap).
+  int W;
   {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     const size_t avail = fr + c->ws_bytes;
     const size_t cap = (size_t)(0.85 * (double)avail) / slot_bytes;
     if (cap < 1) return fail(c, LIK_ENOMEM, "one workspace slot (%zu bytes) exceeds free HBM", slot_bytes);
-    if ((size_t)W > cap) W = (int)cap;
+    if (c->wave_points > 0) {
+      W = (int)std::min<size_t>((size_t)std::min(c->wave_points, K), cap);
+    } else {
+      const size_t half = std::max<size_t>(1, (size_t)(0.5 * (double)avail) / slot_bytes);
+      const int wmax = (int)std::min<size_t>((size_t)16 * c->nsm * lik::chol_ctas_per_sm(), half);
+      const int nw = (K + wmax - 1) / wmax;
+      W = (K + nw - 1) / nw;
+    }
   }
+  tr.mark("memgetinfo");
   int rc;
   if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes))) return rc;
   size_t pcb = c->pc_cap * sizeof(PointConst);
@@ -212,6 +240,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     return rc;
 
   if ((rc = ensure(c, &c->coords_p, &c->coords_p_bytes, (size_t)n * 2 * sizeof(double)))) return rc;
+  tr.mark("ensure");
   const int* dperm = nullptr;
   if (!(c->flags & LIK_FLAG_NATURAL_ORDER)) {
     morton_order(n, hcoords, c->hperm);
@@ -220,6 +249,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
                                 cudaMemcpyHostToDevice, st));
     dperm = c->perm;
   }
+  tr.mark("morton+h2d");
 
   const bool timing = c->flags & LIK_FLAG_TIMING;
   const int nwaves = (K + W - 1) / W;
@@ -258,6 +288,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     CUDA_TRY(c, lik::launch_chol(a, kw, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   }
+  tr.mark("launches");
   if (timing) {
     CUDA_TRY(c, cudaEventSynchronize(c->ev[ei - 1]));
     float ms = 0.f;
@@ -353,6 +384,7 @@ int lik_eval_batch_device_ex(lik_ctx* c, int n, int p, const double* coords, con
     return fail(c, LIK_EINVAL, "NULL pointer argument");
   if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || M + p > 64)
     return validate(c, n, p, nullptr, nullptr, nullptr, K, M, nullptr);
+  HostTrace tr;
   CUDA_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   std::vector<double> h((size_t)n * (3 + p) + M);
@@ -365,8 +397,10 @@ int lik_eval_batch_device_ex(lik_ctx* c, int n, int p, const double* coords, con
   CUDA_TRY(c, cudaMemcpyAsync(hX, X, (size_t)n * p * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaMemcpyAsync(hl, lambdas, (size_t)M * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
+  tr.mark("d2h+sync");
   int rc = validate(c, n, p, hc, hy, hX, K, M, hl);
   if (rc) return rc;
+  tr.mark("validate");
   Extras ex;
   ex.detReml = detReml;
   ex.ssqYX = ssqYX;

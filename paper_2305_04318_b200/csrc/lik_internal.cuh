@@ -95,12 +95,13 @@ struct PointConst {
 
 // Per-point Chebyshev table of ln ρ(z) on binary octaves z ∈ [2^e, 2^{e+1}),
 // e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1.  Each octave stores CHEB_STRIDE
-// doubles: a base H_o followed by the CHEB_N monomial coefficients (in
+// doubles: a base H_o, one pad (so the coefficients are 16-byte aligned), then the
+// CHEB_N monomial coefficients (in
 // t = z/2^e·2 − 3 ∈ [−1, 1)) of the degree-19 Chebyshev interpolant of
 // h(z) = ln ρ(z) + z − H_o, so that ln ρ = (H_o + h(z)) − z.  Below 2^CHEB_ELO
 // the exact evaluation is used; at and above 2^e_zero ρ = 0.
 constexpr int CHEB_N = 20;
-constexpr int CHEB_STRIDE = CHEB_N + 1;
+constexpr int CHEB_STRIDE = CHEB_N + 2;
 constexpr int CHEB_ELO = -26;
 constexpr int CHEB_NOCT = 40;
 constexpr int TABLE_D = CHEB_STRIDE * CHEB_NOCT;

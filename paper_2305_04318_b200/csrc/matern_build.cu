@@ -180,12 +180,12 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   __syncthreads();
   double* T = table + (size_t)blockIdx.x * TABLE_D;
   for (int idx = tid; idx < CHEB_NOCT * CHEB_STRIDE; idx += 256) {
-    const int o = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 1;
+    const int o = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 2;
     double a = 0.0;
     if (CHEB_ELO + o < ez) {
-      if (kk < 0) {
+      if (kk == -2) {
         a = f[o * CHEB_N + CHEB_N / 2];  // H_o
-      } else {
+      } else if (kk >= 0) {
         for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[o * CHEB_N + jj] * tco[jj * CHEB_N + kk];
       }
     }
@@ -217,7 +217,9 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
   if (P.mode == MODE_BAD) return;
   const int npad = g.nt * TB;
   __shared__ double sx[2][TB], sy[2][TB];
-  __shared__ double coef[TABLE_D];
+  __shared__ __align__(16) double coef[TABLE_D];
+  __shared__ double etab[32];
+  if (threadIdx.x < 32) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
   if (P.mode == MODE_BESSEL) {
     const double* src = table + (size_t)slot * TABLE_D;
     const int nval = min(CHEB_NOCT, max(0, P.e_zero - CHEB_ELO)) * CHEB_STRIDE;
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(256) build_kernel(const double* __restrict__ c
       for (int q = 0; q < 16; q += 2) {
         const int ra = r0 + 4 * q, rb = ra + 4;
         double va, vb;
-        matern_rho_table2(P, coef, sx[0][ra] - xj, sy[0][ra] - yj, sx[0][rb] - xj, sy[0][rb] - yj,
+        matern_rho_table2(P, coef, etab, sx[0][ra] - xj, sy[0][ra] - yj, sx[0][rb] - xj, sy[0][rb] - yj,
                           va, vb, slow, q);
         T[sw_off(ra, c)] = va;
         T[sw_off(rb, c)] = vb;

@@ -65,6 +65,8 @@ def test_matern_build_elementwise(ctx, orc, name):
     P[1, 1] = 0.5
     P[2, 1] = 2000.0    # Gaussian limit (R7)
     P[3, 1] = 0.21
+    # large κ at long range: ln ρ far below −746 inside the last non-zero table octave
+    P[4] = [40751.846, 230.364234, 1.22954009, 4.43248760, 0.496259428]
     dc = torch.tensor(coords, device="cuda")
     dp = torch.tensor(P, device="cuda")
     V = ctx.debug_build_V(dc, dp).cpu().numpy()

@@ -33,6 +33,21 @@ class Recorder:
         return r
 
 
+def assert_status_or_borderline(orc, coords, params, st_g, st_r):
+    """Statuses must agree, except where the R11 non-PD decision (pivot ≤ n·ε·max V_ii,
+    P:853) sits within rounding of its threshold: nugget-repaired points (ν² = 0,
+    P:277) with long ranges give nearly singular V, and the two sides factor it by
+    different FP64 algorithms (blocked LLᵀ vs unblocked LDLᵀ, R10), so a pivot within
+    a few n·ε·‖V‖ of the threshold may land on either side."""
+    n = coords.shape[0]
+    for i in np.nonzero(st_g != st_r)[0]:
+        assert {int(st_g[i]), int(st_r[i])} == {lik.PT_OK, lik.PT_V_NOT_PD}, (i, st_g[i], st_r[i])
+        _, D, _ = orc.ldl(orc.build_V(coords, params[i]))
+        tol = n * np.finfo(float).eps * (1.0 + params[i][2])
+        dmin = D[D != 0].min() if np.any(D != 0) else 0.0
+        assert dmin < 100 * tol, (i, params[i], dmin / tol)
+
+
 @pytest.fixture(scope="module")
 def ctx():
     c = lik.create(0)
@@ -90,8 +105,9 @@ def test_representative_pipeline_profiles(ctx, orc):
     assert np.mean(res["status"] == 0) > 0.95
     sel = np.random.default_rng(0).choice(len(rs.params), 24, replace=False)
     ref = orc.eval_batch(coords, y, X, rs.params[sel], rs.lambdas, nthreads=NTHREADS)
-    assert np.array_equal(res["status"][sel], ref["status"])
-    ok = ref["status"] == 0
+    st_g = res["status"][sel]
+    assert_status_or_borderline(orc, coords, rs.params[sel], st_g, ref["status"])
+    ok = (ref["status"] == 0) & (st_g == 0)
     rel = np.abs(res["loglik"][sel][ok] - ref["loglik"][ok]) / np.abs(ref["loglik"][ok])
     assert rel.max() <= 1e-8
     # λ profile: max over points of ℓ_p(ω_k, λ_m), then the CI
