@@ -353,10 +353,11 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
     for (int q = 0; q < NSTAGE && q < nq; ++q) issue(q);
 #ifndef LIK_NO_SWP
   if (mlim == 4) {
-    // Software-pipelined full-tile path: the fragments of k-step t+1 (and, at a
-    // chunk's last k-step, the first fragments of the next chunk, after waiting on
-    // its full barrier) are loaded before the 16 DMMAs of k-step t are issued, so
-    // the shared-memory latency is off the DMMA issue chain.
+    // Software-pipelined full-tile path: the fragments of k-step t+1 are loaded
+    // before the 16 DMMAs of k-step t are issued; the next chunk's first fragments
+    // after the stage is released and its full barrier completes.  (Loading them
+    // before the last k-step — blocking or with a non-blocking probe — measured
+    // slower.)
     const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
     const int aoff = mine_b ? CHUNK_D : 0;
     double fa[2][4], fb[2][4];
@@ -387,12 +388,6 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
         if (kk + 1 < KC / 4) {
           load(fa[cur ^ 1], fb[cur ^ 1], st, kk + 1);
         }
-#ifdef LIK_SWP_CROSS
-        else if (q + 1 < nq) {
-          wait_full(q + 1);
-          load(fa[cur ^ 1], fb[cur ^ 1], stage_of(q + 1), 0);
-        }
-#endif
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -400,12 +395,10 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(saddr(&pp.empty[(seq + q) % NSTAGE]));
-#ifndef LIK_SWP_CROSS
       if (q + 1 < nq) {
         wait_full(q + 1);
         load(fa[0], fb[0], stage_of(q + 1), 0);
       }
-#endif
     }
     pp.seq = seq + nq;
     return;
