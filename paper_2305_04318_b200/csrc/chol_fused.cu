@@ -435,17 +435,133 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
   pp.seq = seq + nq;
 }
 
+// 32×32 scratch (T): two swizzled 32×16 halves, the chunk layout's bank pattern.
+__device__ __forceinline__ int t_off(int r, int c) {
+  return (c >> 4) * 512 + r * 16 + ((c & 15) ^ ((r & 3) << 2));
+}
+
+#ifndef LIK_PW
+#define LIK_PW 8
+#endif
+constexpr int PW = LIK_PW;  // panel width of the diagonal-tile factorisation (8 or 16)
+static_assert(PW == 8 || PW == 16, "panel width");
+
+// Step (a) of a panel at c0 (the lead warp): factor the PW×PW diagonal block D_p in
+// registers — lane l holds row l; one rsqrt per pivot gives L_cc and 1/L_cc, and
+// the update of the trailing columns uses the pivot column fetched by shuffles —
+// then invert it (lane l computes column l of D_p⁻¹, right-looking, so the
+// dependent chain is two ops per step).  Only the pivot chain is serial; it uses no
+// divisions (the FP64 pipe is shared with the co-resident CTA's DMMAs, so every
+// dependent FP64 op on it is slow).  Pivots ≥ vloc are skipped (their rows and
+// columns of D_p⁻¹ are 0).  dlog[c0 + c] = log(pivot_c); a pivot ≤ tol sets flag[0].
+__device__ __forceinline__ void factor_block(double* S, double* X, int c0, int vloc, double tol,
+                                             double* dlog, int* flag) {
+  const int lane = threadIdx.x & 31, l = lane & (PW - 1);
+  double a[PW];
+#pragma unroll
+  for (int k = 0; k < PW; ++k) a[k] = (k <= l) ? S[sw_off(c0 + l, c0 + k)] : 0.0;
+  int bad = 0;
+  double my_piv = 1.0, my_rinv = 1.0;
+#pragma unroll
+  for (int c = 0; c < PW; ++c) {
+    if (c < vloc) {
+      const double piv = __shfl_sync(0xffffffffu, a[c], c);
+      bad |= !(piv > tol);
+      const double rinv = rsqrt(piv);
+      if (l == c) {
+        a[c] = piv * rinv;
+        my_piv = piv;
+        my_rinv = rinv;
+      } else if (l > c) {
+        a[c] *= rinv;
+      }
+#pragma unroll
+      for (int k = 0; k < PW; ++k) {  // constant trip count: a[] stays in registers
+        if (k > c) {
+          const double lk = __shfl_sync(0xffffffffu, a[c], k);
+          if (l >= k) a[k] -= a[c] * lk;
+        }
+      }
+    }
+  }
+  if (lane < PW && l < vloc) dlog[c0 + l] = log(my_piv);
+  double x[PW];
+#pragma unroll
+  for (int i = 0; i < PW; ++i) x[i] = (i == l && l < vloc) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < PW; ++i) {
+    if (i < vloc) {
+      x[i] *= __shfl_sync(0xffffffffu, my_rinv, i);
+#pragma unroll
+      for (int k = 0; k < PW; ++k)
+        if (k > i) x[k] -= __shfl_sync(0xffffffffu, a[i], k) * x[i];
+    }
+  }
+  if (lane < PW) {
+#pragma unroll
+    for (int k = 0; k < PW; ++k) {
+      if (k <= l) S[sw_off(c0 + l, c0 + k)] = a[k];
+      X[sw_off(c0 + k, c0 + l)] = (k < vloc && l < vloc) ? x[k] : 0.0;  // column l of D_p⁻¹
+    }
+  }
+  if (lane == 0 && bad) flag[0] = 1;
+}
+
+// Steps (b) and (c) of the panel at c0 of the tile S (swizzled), with D_p⁻¹ in X, on
+// the FP64 tensor cores:
+//   (b) L[i, panel] = S[i, panel] · D_p⁻ᵀ   for rows i ∈ [c0+PW, 64): warp w owns rows
+//       c0+PW+8w..+7 (all column tiles), so the in-place store needs no barrier;
+//   (c) S[i, k] −= L[i, panel] · L[k, panel]ᵀ  for the 8×8 tiles on/below the diagonal
+//       of [c0+PW, 64)², one warp per tile.
+// DMMA fragments (m8n8k4): a = A[r + lane/4][k + lane%4], b = B[k + lane%4][n + lane/4],
+// c = C[r + lane/4][n + 2(lane%4) + {0,1}].
+__device__ void panel_update(double* S, const double* X, int c0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lr = lane >> 2, lc = lane & 3;
+  const int b0 = c0 + PW, rt = (TB - b0) >> 3;
+  if (warp < rt) {
+    const int r = b0 + 8 * warp;
+    double c[PW / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < PW / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < PW / 4; ++ks) {
+      const double a = S[sw_off(r + lr, c0 + 4 * ks + lc)];
+#pragma unroll
+      for (int nt = 0; nt < PW / 8; ++nt) {
+        if (4 * ks > 8 * nt + 7) continue;  // D_p⁻¹ is lower triangular
+        dmma(c[nt], a, X[sw_off(c0 + 8 * nt + lr, c0 + 4 * ks + lc)]);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < PW / 8; ++nt)
+      *reinterpret_cast<double2*>(S + sw_off(r + lr, c0 + 8 * nt + 2 * lc)) = make_double2(c[nt][0], c[nt][1]);
+  }
+  __syncthreads();
+  const int ntile = rt * (rt + 1) / 2;
+  for (int t = warp; t < ntile; t += NT / 32) {
+    int ti = 0;
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    const int ri = b0 + 8 * ti, rk = b0 + 8 * (t - ti * (ti + 1) / 2);
+    double c[2] = {0.0, 0.0};
+#pragma unroll
+    for (int ks = 0; ks < PW / 4; ++ks)
+      dmma(c, S[sw_off(ri + lr, c0 + 4 * ks + lc)], S[sw_off(rk + lr, c0 + 4 * ks + lc)]);
+    double2* q = reinterpret_cast<double2*>(S + sw_off(ri + lr, rk + 2 * lc));
+    const double2 o = *q;
+    *q = make_double2(o.x - c[0], o.y - c[1]);
+  }
+  __syncthreads();
+}
+
 // Blocked Cholesky + inverse of a 64×64 tile in shared memory (lower part used)
-// whose rows/columns ≥ v are the identity padding of V.  Four 16-column panels:
-//   (a) warp 0 factors the 16×16 diagonal block D_p in registers (shuffles) and
-//       inverts it into X (the diagonal blocks of L⁻¹),
-//   (b) the rows below: L[i, panel] = S[i, panel] · D_p⁻ᵀ (parallel products),
-//   (c) trailing update of the lower triangle with the panel (parallel).
-// Then L⁻¹ is assembled from the D_p⁻¹ by block recursion (16 → 32 → 64):
-//   X_ba = −X_bb (L_ba X_aa)  for the off-diagonal blocks.
-// Every step is a short product with ≤ 32-long dot products, so the phase has no
-// long dependent chains.  dlog[c] = log(pivot_c).  Returns nonzero (uniformly)
-// if a pivot is ≤ tol (R11).  T is a 32×32 scratch.
+// whose rows/columns ≥ v are the identity padding of V.  64/PW panels:
+//   (a) the lead warp factors the PW×PW diagonal block D_p and inverts it into X
+//       (the diagonal blocks of L⁻¹) — factor_block,
+//   (b)+(c) panel product and trailing update on the tensor cores — panel_update.
+// Then L⁻¹ is assembled from the D_p⁻¹ by block recursion (PW → … → 64) on the
+// tensor cores:  X_ba = −X_bb (L_ba X_aa)  for the off-diagonal blocks.
+// dlog[c] = log(pivot_c).  Returns nonzero (uniformly) if a pivot is ≤ tol (R11).
+// T is a 32×32 scratch.
 #ifdef LIK_PHASE_TIMERS
 #define SUB(i) do { if (threadIdx.x == 224) { const long long t_ = clock64(); atomicAdd(&g_lik_phase[i], (unsigned long long)(t_ - sub_t)); sub_t = t_; } } while (0)
 #else
@@ -464,142 +580,95 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     }
     __syncthreads();
   }
-  for (int c0 = 0; c0 < TB; c0 += 16) {
-    if (warp == LEAD_WARP) {
-      // Only the pivot chain is serial: one rsqrt per pivot gives L_cc and 1/L_cc;
-      // logs and the inverse use no divisions (the FP64 pipe is shared with the
-      // co-resident CTA's DMMAs, so every dependent FP64 op on this chain is slow).
-      const int l = lane & 15;
-      double a[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = (k <= l) ? S[sw_off(c0 + l, c0 + k)] : 0.0;
-      int bad = 0;
-      double my_piv = 1.0, my_rinv = 1.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const double piv = __shfl_sync(0xffffffffu, a[c], c);
-        bad |= !(piv > tol);
-        const double rinv = rsqrt(piv);
-        if (l == c) {
-          a[c] = piv * rinv;
-          my_piv = piv;
-          my_rinv = rinv;
-        } else if (l > c) {
-          a[c] *= rinv;
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {  // constant trip count: fully unrolled, a[] stays in registers
-          if (k > c) {
-            const double lk = __shfl_sync(0xffffffffu, a[c], k);
-            if (l >= k) a[k] -= a[c] * lk;
-          }
-        }
-      }
-      if (lane < 16) dlog[c0 + l] = log(my_piv);
-      // lane l computes column l of D_p⁻¹, right-looking: x = e_l; for each i,
-      // x_i *= 1/D_ii, then x_k −= D_ki x_i for k > i (independent updates, so the
-      // dependent chain is two ops per step).  D_ki is fetched from lane k.
-      double x[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = (i == l) ? 1.0 : 0.0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        x[i] *= __shfl_sync(0xffffffffu, my_rinv, i);
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (k > i) x[k] -= __shfl_sync(0xffffffffu, a[i], k) * x[i];
-      }
-      if (lane < 16) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          if (k <= l) S[sw_off(c0 + l, c0 + k)] = a[k];
-          X[sw_off(c0 + k, c0 + l)] = x[k];  // column l of D_p⁻¹
-        }
-      }
-      if (lane == 0 && bad) flag[0] = 1;
-    }
+  for (int c0 = 0; c0 < TB; c0 += PW) {
+    if (warp == LEAD_WARP) factor_block(S, X, c0, PW, tol, dlog, flag);
     SUB(10);
     __syncthreads();
     SUB(11);
 #ifndef LIK_EXP_SAMESRC
     if (flag[0]) return 1;
 #endif
-    if (c0 + 16 < TB) {
-      // (b) L[i, c0+c] = Σ_{k ≤ c} S[i, c0+k] · D_p⁻¹[c][k]  (rows below the panel)
-      const int base = c0 + 16, m = TB - base;
-      double xv[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int e = tid + q * NT;
-        xv[q] = 0.0;
-        if (e < m * 16) {
-          const int i = base + (e >> 4), c = e & 15;
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < 16; ++k)
-            if (k <= c) s += S[sw_off(i, c0 + k)] * X[sw_off(c0 + c, c0 + k)];
-          xv[q] = s;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int e = tid + q * NT;
-        if (e < m * 16) S[sw_off(base + (e >> 4), c0 + (e & 15))] = xv[q];
-      }
-      __syncthreads();
-      SUB(12);
-      // (c) trailing update of the lower triangle below/right of the panel
-      for (int e = tid; e < m * m; e += NT) {
-        const int i = base + e / m, kk = base + e % m;
-        if (kk <= i) {
-          double s = S[sw_off(i, kk)];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) s -= S[sw_off(i, c0 + c)] * S[sw_off(kk, c0 + c)];
-          S[sw_off(i, kk)] = s;
-        }
-      }
-      __syncthreads();
+    if (c0 + PW < TB) {
+      panel_update(S, X, c0);
       SUB(13);
     }
   }
-  // strictly-upper parts of X are zero
+  // strictly-upper parts of X (above the PW-blocks on its diagonal) are zero
   for (int e = tid; e < TILE_D; e += NT) {
     const int i = e >> 6, c = e & 63;
-    if ((c >> 4) > (i >> 4)) X[sw_off(i, c)] = 0.0;
+    if (c / PW > i / PW) X[sw_off(i, c)] = 0.0;
   }
-  // L⁻¹ off-diagonal blocks, level 16 → 32: blocks (1,0) of each 32-block
-  for (int e = tid; e < 2 * 256; e += NT) {  // T_h = L_{(2h+1),(2h)} X_{(2h),(2h)}
-    const int h = e >> 8, i = (e >> 4) & 15, c = e & 15, o = 32 * h;
-    double s = 0.0;
+  __syncthreads();
+  if (PW == 8) {  // level 8 → 16: X_{(2g+1),(2g)} = −X_{(2g+1),(2g+1)} (L_{(2g+1),(2g)} X_{(2g),(2g)})
+    const int lr = lane >> 2, lc = lane & 3, o = 16 * warp;
+    if (warp < 4) {
+      double c[2] = {0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k >= c) s += S[sw_off(o + 16 + i, o + k)] * X[sw_off(o + k, o + c)];
-    T[e] = s;
-  }
-  __syncthreads();
-  for (int e = tid; e < 2 * 256; e += NT) {  // X_{(2h+1),(2h)} = −X_{(2h+1),(2h+1)} T_h
-    const int h = e >> 8, i = (e >> 4) & 15, c = e & 15, o = 32 * h;
-    double s = 0.0;
+      for (int ks = 0; ks < 2; ++ks)
+        dmma(c, S[sw_off(o + 8 + lr, o + 4 * ks + lc)], X[sw_off(o + 4 * ks + lc, o + lr)]);
+      T[t_off(8 * warp + lr, 2 * lc)] = c[0];
+      T[t_off(8 * warp + lr, 2 * lc + 1)] = c[1];
+    }
+    __syncthreads();
+    if (warp < 4) {
+      double c[2] = {0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k <= i) s += X[sw_off(o + 16 + i, o + 16 + k)] * T[h * 256 + k * 16 + c];
-    X[sw_off(o + 16 + i, o + c)] = -s;
+      for (int ks = 0; ks < 2; ++ks)
+        dmma(c, X[sw_off(o + 8 + lr, o + 8 + 4 * ks + lc)], T[t_off(8 * warp + 4 * ks + lc, lr)]);
+      *reinterpret_cast<double2*>(X + sw_off(o + 8 + lr, o + 2 * lc)) = make_double2(-c[0], -c[1]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // level 32 → 64: X21 = −X22 (L21 X11)
-  for (int e = tid; e < 1024; e += NT) {
-    const int i = e >> 5, c = e & 31;
-    double s = 0.0;
-    for (int k = c; k < 32; ++k) s += S[sw_off(32 + i, k)] * X[sw_off(k, c)];
-    T[e] = s;
-  }
-  __syncthreads();
-  for (int e = tid; e < 1024; e += NT) {
-    const int i = e >> 5, c = e & 31;
-    double s = 0.0;
-    for (int k = 0; k <= i; ++k) s += X[sw_off(32 + i, 32 + k)] * T[k * 32 + c];
-    X[sw_off(32 + i, c)] = -s;
+  // L⁻¹ off-diagonal blocks by block recursion on the tensor cores, one 8×8 tile per
+  // warp: level 16 → 32 (blocks (1,0) of each 32-block), then 32 → 64.
+  {
+    const int lr = lane >> 2, lc = lane & 3;
+    const int h = warp >> 2, i0 = ((warp >> 1) & 1) * 8, n0 = (warp & 1) * 8, o = 32 * h;
+    double c[2] = {0.0, 0.0};
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {  // T_h = L_{(2h+1),(2h)} X_{(2h),(2h)}  (X lower: k ≥ n)
+      if (4 * ks + 3 < n0) continue;
+      dmma(c, S[sw_off(o + 16 + i0 + lr, o + 4 * ks + lc)], X[sw_off(o + 4 * ks + lc, o + n0 + lr)]);
+    }
+    T[t_off(16 * h + i0 + lr, n0 + 2 * lc)] = c[0];
+    T[t_off(16 * h + i0 + lr, n0 + 2 * lc + 1)] = c[1];
+    __syncthreads();
+    c[0] = c[1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {  // X_{(2h+1),(2h)} = −X_{(2h+1),(2h+1)} T_h  (k ≤ i)
+      if (4 * ks > i0 + 7) continue;
+      dmma(c, X[sw_off(o + 16 + i0 + lr, o + 16 + 4 * ks + lc)], T[t_off(16 * h + 4 * ks + lc, n0 + lr)]);
+    }
+    *reinterpret_cast<double2*>(X + sw_off(o + 16 + i0 + lr, o + n0 + 2 * lc)) = make_double2(-c[0], -c[1]);
+    __syncthreads();
+    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {  // level 32 → 64: T = L21 X11  (two tiles per warp)
+      const int tile = warp + 8 * u, r0 = (tile >> 2) * 8, m0 = (tile & 3) * 8;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        if (4 * ks + 3 < m0) continue;
+        dmma(d[u], S[sw_off(32 + r0 + lr, 4 * ks + lc)], X[sw_off(4 * ks + lc, m0 + lr)]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int tile = warp + 8 * u, r0 = (tile >> 2) * 8, m0 = (tile & 3) * 8;
+      T[t_off(r0 + lr, m0 + 2 * lc)] = d[u][0];
+      T[t_off(r0 + lr, m0 + 2 * lc + 1)] = d[u][1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {  // X21 = −X22 T  (k ≤ i)
+      const int tile = warp + 8 * u, r0 = (tile >> 2) * 8, m0 = (tile & 3) * 8;
+      double e[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        if (4 * ks > r0 + 7) continue;
+        dmma(e, X[sw_off(32 + r0 + lr, 32 + 4 * ks + lc)], T[t_off(4 * ks + lc, m0 + lr)]);
+      }
+      *reinterpret_cast<double2*>(X + sw_off(32 + r0 + lr, m0 + 2 * lc)) = make_double2(-e[0], -e[1]);
+    }
   }
   SUB(14);
   return 0;
@@ -611,96 +680,12 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
 // panel product, trailing update), stopping after the last pivot panel: the
 // block rows/cols ≥ off then hold C_BB − Z Zᵀ = −BᵀV⁻¹B (the Schur complement).
 __device__ int potrf_tail(double* S, int v, double tol, double* dlog, int* flag, double* X) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int c0 = 0; c0 < v; c0 += 16) {
-    const int vloc = min(16, v - c0);
-    if (warp == LEAD_WARP) {
-      const int l = lane & 15;
-      double a[16];
-#pragma unroll
-      for (int kk = 0; kk < 16; ++kk) a[kk] = (kk <= l) ? S[sw_off(c0 + l, c0 + kk)] : 0.0;
-      int bad = 0;
-      double my_piv = 1.0, my_rinv = 1.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c < vloc) {
-          const double piv = __shfl_sync(0xffffffffu, a[c], c);
-          bad |= !(piv > tol);
-          const double rinv = rsqrt(piv);
-          if (l == c) {
-            a[c] = piv * rinv;
-            my_piv = piv;
-            my_rinv = rinv;
-          } else if (l > c) {
-            a[c] *= rinv;
-          }
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            if (kk > c) {
-              const double lk = __shfl_sync(0xffffffffu, a[c], kk);
-              if (l >= kk) a[kk] -= a[c] * lk;
-            }
-          }
-        }
-      }
-      if (lane < 16 && l < vloc) dlog[c0 + l] = log(my_piv);
-      double x[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = (i == l && l < vloc) ? 1.0 : 0.0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (i < vloc) {
-          x[i] *= __shfl_sync(0xffffffffu, my_rinv, i);
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk)
-            if (kk > i) x[kk] -= __shfl_sync(0xffffffffu, a[i], kk) * x[i];
-        }
-      }
-      if (lane < 16) {
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          if (kk <= l) S[sw_off(c0 + l, c0 + kk)] = a[kk];
-          X[sw_off(c0 + kk, c0 + l)] = (kk < vloc && l < vloc) ? x[kk] : 0.0;
-        }
-      }
-      if (lane == 0 && bad) flag[0] = 1;
-    }
+  const int warp = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < v; c0 += PW) {
+    if (warp == LEAD_WARP) factor_block(S, X, c0, min(PW, v - c0), tol, dlog, flag);
     __syncthreads();
     if (flag[0]) return 1;
-    if (c0 + 16 < TB) {
-      const int base = c0 + 16, m = TB - base;
-      double xv[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int e = tid + q * NT;
-        xv[q] = 0.0;
-        if (e < m * 16) {
-          const int i = base + (e >> 4), c = e & 15;
-          double acc1 = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk)
-            if (kk <= c) acc1 += S[sw_off(i, c0 + kk)] * X[sw_off(c0 + c, c0 + kk)];
-          xv[q] = acc1;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int e = tid + q * NT;
-        if (e < m * 16) S[sw_off(base + (e >> 4), c0 + (e & 15))] = xv[q];
-      }
-      __syncthreads();
-      for (int e = tid; e < m * m; e += NT) {
-        const int i = base + e / m, kk = base + e % m;
-        if (kk <= i) {
-          double acc1 = S[sw_off(i, kk)];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) acc1 -= S[sw_off(i, c0 + c)] * S[sw_off(kk, c0 + c)];
-          S[sw_off(i, kk)] = acc1;
-        }
-      }
-      __syncthreads();
-    }
+    if (c0 + PW < TB) panel_update(S, X, c0);
   }
   return 0;
 }
