@@ -515,7 +515,7 @@ __device__ __forceinline__ void factor_block(double* S, double* X, int c0, int v
 //       of [c0+PW, 64)², one warp per tile.
 // DMMA fragments (m8n8k4): a = A[r + lane/4][k + lane%4], b = B[k + lane%4][n + lane/4],
 // c = C[r + lane/4][n + 2(lane%4) + {0,1}].
-__device__ void panel_update(double* S, const double* X, int c0) {
+__device__ __forceinline__ void panel_product(double* S, const double* X, int c0) {  // (b)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lr = lane >> 2, lc = lane & 3;
   const int b0 = c0 + PW, rt = (TB - b0) >> 3;
   if (warp < rt) {
@@ -536,20 +536,29 @@ __device__ void panel_update(double* S, const double* X, int c0) {
     for (int nt = 0; nt < PW / 8; ++nt)
       *reinterpret_cast<double2*>(S + sw_off(r + lr, c0 + 8 * nt + 2 * lc)) = make_double2(c[nt][0], c[nt][1]);
   }
-  __syncthreads();
-  const int ntile = rt * (rt + 1) / 2;
-  for (int t = warp; t < ntile; t += NT / 32) {
-    int ti = 0;
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    const int ri = b0 + 8 * ti, rk = b0 + 8 * (t - ti * (ti + 1) / 2);
-    double c[2] = {0.0, 0.0};
+}
+
+// (c) for tile t of the lower triangle of [c0+PW, 64)² in 8×8 tiles (t = 0: the
+// next diagonal block).
+__device__ __forceinline__ void trailing_tile(double* S, int c0, int t) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3, b0 = c0 + PW;
+  int ti = 0;
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  const int ri = b0 + 8 * ti, rk = b0 + 8 * (t - ti * (ti + 1) / 2);
+  double c[2] = {0.0, 0.0};
 #pragma unroll
-    for (int ks = 0; ks < PW / 4; ++ks)
-      dmma(c, S[sw_off(ri + lr, c0 + 4 * ks + lc)], S[sw_off(rk + lr, c0 + 4 * ks + lc)]);
-    double2* q = reinterpret_cast<double2*>(S + sw_off(ri + lr, rk + 2 * lc));
-    const double2 o = *q;
-    *q = make_double2(o.x - c[0], o.y - c[1]);
-  }
+  for (int ks = 0; ks < PW / 4; ++ks)
+    dmma(c, S[sw_off(ri + lr, c0 + 4 * ks + lc)], S[sw_off(rk + lr, c0 + 4 * ks + lc)]);
+  double2* q = reinterpret_cast<double2*>(S + sw_off(ri + lr, rk + 2 * lc));
+  const double2 o = *q;
+  *q = make_double2(o.x - c[0], o.y - c[1]);
+}
+
+__device__ void panel_update(double* S, const double* X, int c0) {  // (b) then (c), all warps
+  panel_product(S, X, c0);
+  __syncthreads();
+  const int rt = (TB - c0 - PW) >> 3;
+  for (int t = threadIdx.x >> 5; t < rt * (rt + 1) / 2; t += NT / 32) trailing_tile(S, c0, t);
   __syncthreads();
 }
 
@@ -580,18 +589,32 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     }
     __syncthreads();
   }
-  for (int c0 = 0; c0 < TB; c0 += PW) {
-    if (warp == LEAD_WARP) factor_block(S, X, c0, PW, tol, dlog, flag);
-    SUB(10);
+  // Lookahead: after the panel product of panel p, the lead warp updates the next
+  // diagonal block (trailing tile 0) and factors it at once, while the other warps
+  // update the rest of the trailing matrix (disjoint tiles).
+  if (warp == LEAD_WARP) factor_block(S, X, 0, PW, tol, dlog, flag);
+  SUB(10);
+  __syncthreads();
+  SUB(11);
+#ifndef LIK_EXP_SAMESRC
+  if (flag[0]) return 1;
+#endif
+  for (int c0 = 0; c0 + PW < TB; c0 += PW) {
+    panel_product(S, X, c0);
     __syncthreads();
-    SUB(11);
+    const int rt = (TB - c0 - PW) >> 3, ntile = rt * (rt + 1) / 2;
+    if (warp == LEAD_WARP) {
+      trailing_tile(S, c0, 0);
+      __syncwarp();
+      factor_block(S, X, c0 + PW, PW, tol, dlog, flag);
+    } else {
+      for (int t = 1 + warp; t < ntile; t += NT / 32 - 1) trailing_tile(S, c0, t);
+    }
+    __syncthreads();
+    SUB(13);
 #ifndef LIK_EXP_SAMESRC
     if (flag[0]) return 1;
 #endif
-    if (c0 + PW < TB) {
-      panel_update(S, X, c0);
-      SUB(13);
-    }
   }
   // strictly-upper parts of X (above the PW-blocks on its diagonal) are zero
   for (int e = tid; e < TILE_D; e += NT) {
