@@ -162,7 +162,8 @@ int lik_get_stage_times(lik_ctx* ctx, double* ms, long long* launches);
 int lik_reset_stage_times(lik_ctx* ctx);
 
 /* Points per wave, i.e. per build/factor launch (0 = automatic: the fewest
- * balanced waves of at most 16 × (2 × #SMs) points within half the free HBM;
+ * waves of at most 16 × (2 × #SMs) points within half the free HBM, each a
+ * multiple of 2 × #SMs except the last;
  * an explicit value is capped at 85 % of free HBM).  The workspace holds one
  * slot per wave point (C4: 17.9 MB).  Results do not depend on it
  * (determinism tests). */

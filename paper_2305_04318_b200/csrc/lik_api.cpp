@@ -209,8 +209,9 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   // Wave size W (points per table/build/chol launch).  All CTAs of a chol launch
   // start together and the launch ends with its slowest point, so fewer, larger
   // launches lose less to that tail (the CTA scheduler backfills within a launch):
-  // by default the fewest balanced waves of at most 16 × (resident CTAs per GPU)
-  // points that fit in half the free HBM.  lik_set_wave_points overrides (85 % cap).
+  // by default the fewest waves of at most 16 × (resident CTAs per GPU) points that
+  // fit in half the free HBM, each a whole number of CTA rounds except the last.
+  // lik_set_wave_points overrides (85 % cap).
   int W;
   {
     size_t fr = 0, tot = 0;
@@ -221,10 +222,15 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     if (c->wave_points > 0) {
       W = (int)std::min<size_t>((size_t)std::min(c->wave_points, K), cap);
     } else {
+      // waves are whole multiples of the resident CTAs (res), so only the last
+      // launch ends on a partly filled round
+      const int res = c->nsm * lik::chol_ctas_per_sm();
       const size_t half = std::max<size_t>(1, (size_t)(0.5 * (double)avail) / slot_bytes);
-      const int wmax = (int)std::min<size_t>((size_t)16 * c->nsm * lik::chol_ctas_per_sm(), half);
+      int wmax = (int)std::min<size_t>((size_t)16 * res, half);
+      if (wmax >= res) wmax -= wmax % res;
       const int nw = (K + wmax - 1) / wmax;
       W = (K + nw - 1) / nw;
+      if (W > res) W = std::min({wmax, (W + res - 1) / res * res, K});
     }
   }
   tr.mark("memgetinfo");
