@@ -116,107 +116,91 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;\n" ::: "memory");
 }
 
-typedef double Acc[4][4][2];
+// Warp tile: 16 rows × 64 columns (full rows of the 128×64 row block), as MI = 2
+// row groups × NI = 8 column groups of 8×8 DMMA accumulators.  Owning full rows
+// lets the triangular solve L = C·L_jj⁻ᵀ run from the warp's own registers.
+constexpr int MI = 2, NI = 8;
+typedef double Acc[MI][NI][2];
 
-// One 64×16 chunk (4 k-steps of 4) of  acc += A_rows · B_rowsᵀ  for this warp.
-// MFULL: all four 8-row subtiles of the warp are live (the common case), so the
-// DMMA sequence is branch- and predicate-free.
+// One chunk (KC/4 k-steps of 4) of  acc += A_rows · B_rowsᵀ  for this warp.
+// MFULL: both 8-row groups of the warp are live (the common case), so the DMMA
+// sequence is branch- and predicate-free.
 template <bool MFULL>
 __device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ Ab, int rbase,
-                                          int mlim, const double* __restrict__ Bb, int cbase,
-                                          int lane) {
+                                          int mlim, const double* __restrict__ Bb, int lane) {
   const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
 #pragma unroll
   for (int kk = 0; kk < KC / 4; ++kk) {
     const int kcol = ((kk * 4) ^ sw) + lc;
-    double a[4], b[4];
+    double a[MI], b[NI];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
+    for (int mi = 0; mi < MI; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = Bb[(cbase + ni * 8 + lr) * KC + kcol];
-    if (MFULL) {
+    for (int ni = 0; ni < NI; ++ni) b[ni] = Bb[(ni * 8 + lr) * KC + kcol];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
+      if (MFULL || mi < mlim) {
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
-    } else {
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-        if (mi < mlim) {
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
-        }
-    }
+        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
   }
 }
 
 __device__ __forceinline__ void mma_chunk_any(Acc& acc, const double* Ab, int rbase, int mlim,
-                                              const double* Bb, int cbase, int lane) {
-  if (mlim == 4)
-    mma_chunk<true>(acc, Ab, rbase, 4, Bb, cbase, lane);
+                                              const double* Bb, int lane) {
+  if (mlim == MI)
+    mma_chunk<true>(acc, Ab, rbase, MI, Bb, lane);
   else if (mlim > 0)
-    mma_chunk<false>(acc, Ab, rbase, mlim, Bb, cbase, lane);
+    mma_chunk<false>(acc, Ab, rbase, mlim, Bb, lane);
 }
 
-// acc = C · L⁻ᵀ for this warp's 32×32 tile (C rows in shared memory, 64 columns in
-// CHUNKS chunks; X = L⁻¹ lower triangular).  (C L⁻ᵀ)[r][c] = Σ_{k ≤ c} C[r][k] X[c][k],
-// so DMMA k-steps entirely above the warp's columns are skipped (compile time, WC =
-// warp column block): half the multiply-adds of the dense product.
-template <int WC, bool MFULL>
-__device__ __forceinline__ void trsm_tri(Acc& acc, const double* __restrict__ Sb, int rbase,
-                                         int mlim, const double* __restrict__ X, int lane) {
-  const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
-  constexpr int cb = WC * 32;
+// acc ← acc · Xᵀ in place, X = L⁻¹ (64×64 lower triangular, swizzled shared memory):
+// (C Xᵀ)[r][c] = Σ_{k ≤ c} C[r][k] X[c][k].  The output column group nt needs C's
+// columns ≤ 8nt+7 only, so the groups are produced from the last to the first and
+// each overwrites its own C group once computed.  The A fragment C[r][4s + lane%4]
+// is taken from the accumulator layout (C[r][8t + 2q + e] in lane (r, q), element e)
+// with two shuffles within the lane quad; k-steps above the triangle are skipped.
+__device__ __forceinline__ void trsm_reg(Acc& acc, const double* __restrict__ X, int lane) {
+  const int lr = lane >> 2, lc = lane & 3, quad = lane & ~3, hi = lc >> 1;
+  const bool odd = lc & 1;
 #pragma unroll
-  for (int h = 0; h < CHUNKS; ++h) {
-    if (KC * h > cb + 31) continue;
-    const double* Ab = Sb + h * CHUNK_D;
-    const double* Bb = X + h * CHUNK_D;
+  for (int nt = NI - 1; nt >= 0; --nt) {
+    double o[MI][2];
 #pragma unroll
-    for (int kk = 0; kk < KC / 4; ++kk) {
-      const int k0 = KC * h + 4 * kk;
-      if (k0 > cb + 31) continue;
-      const int kcol = ((kk * 4) ^ sw) + lc;
-      double a[4], b[4];
+    for (int m = 0; m < MI; ++m) o[m][0] = o[m][1] = 0.0;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
+    for (int s = 0; s <= 2 * nt + 1; ++s) {
+      const int src = quad | (2 * (s & 1) + hi);
+      double a[MI];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-        if (cb + ni * 8 + 7 >= k0) b[ni] = Bb[(cb + ni * 8 + lr) * KC + kcol];
+      for (int m = 0; m < MI; ++m) {
+        const double v0 = __shfl_sync(0xffffffffu, acc[m][s >> 1][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, acc[m][s >> 1][1], src);
+        a[m] = odd ? v1 : v0;
+      }
+      const double b = X[sw_off(8 * nt + lr, 4 * s + lc)];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-        if (MFULL || mi < mlim) {
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
-            if (cb + ni * 8 + 7 >= k0) dmma(acc[mi][ni], a[mi], b[ni]);
-        }
+      for (int m = 0; m < MI; ++m) dmma(o[m], a[m], b);
     }
-  }
-}
-
-__device__ __forceinline__ void trsm_any(Acc& acc, const double* Sb, int rbase, int mlim,
-                                         const double* X, int wc, int lane) {
-  if (mlim <= 0) return;
-  if (wc == 0) {
-    if (mlim == 4) trsm_tri<0, true>(acc, Sb, rbase, 4, X, lane);
-    else trsm_tri<0, false>(acc, Sb, rbase, mlim, X, lane);
-  } else {
-    if (mlim == 4) trsm_tri<1, true>(acc, Sb, rbase, 4, X, lane);
-    else trsm_tri<1, false>(acc, Sb, rbase, mlim, X, lane);
+#pragma unroll
+    for (int m = 0; m < MI; ++m) {
+      acc[m][nt][0] = o[m][0];
+      acc[m][nt][1] = o[m][1];
+    }
   }
 }
 
 // acc = acc − T  (T = the A_ij tile in global memory), i.e. −C.
 __device__ __forceinline__ void frag_sub_from(Acc& acc, const double* __restrict__ T, int rbase,
-                                              int cbase, int mlim, int lane) {
+                                              int mlim, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
     if (mi < mlim) {
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const double2 v = *reinterpret_cast<const double2*>(
-            T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc));
+      for (int ni = 0; ni < NI; ++ni) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(T + sw_off(rbase + mi * 8 + lr, ni * 8 + 2 * lc));
         acc[mi][ni][0] -= v.x;
         acc[mi][ni][1] -= v.y;
       }
@@ -226,65 +210,62 @@ __device__ __forceinline__ void frag_sub_from(Acc& acc, const double* __restrict
 // acc −= T (T split: rows < off from T1, rows ≥ off from T2 at row − off)
 __device__ __forceinline__ void frag_sub_from2(Acc& acc, const double* __restrict__ T1,
                                                const double* __restrict__ T2, int off, int rbase,
-                                               int cbase, int mlim, int lane) {
+                                               int mlim, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
     if (mi < mlim) {
       const int row = rbase + mi * 8 + lr;
       const double* T = row < off ? T1 : T2;
       const int rr = row < off ? row : row - off;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const double2 v = *reinterpret_cast<const double2*>(T + sw_off(rr, cbase + ni * 8 + 2 * lc));
+      for (int ni = 0; ni < NI; ++ni) {
+        const double2 v = *reinterpret_cast<const double2*>(T + sw_off(rr, ni * 8 + 2 * lc));
         acc[mi][ni][0] -= v.x;
         acc[mi][ni][1] -= v.y;
       }
     }
 }
 
+template <bool NEG>
 __device__ __forceinline__ void frag_store2(const Acc& acc, double* __restrict__ T1,
-                                            double* __restrict__ T2, int off, int rbase,
-                                            int cbase, int mlim, int lane) {
+                                            double* __restrict__ T2, int off, int rbase, int mlim,
+                                            int lane) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
     if (mi < mlim) {
       const int row = rbase + mi * 8 + lr;
       double* T = row < off ? T1 : T2;
       const int rr = row < off ? row : row - off;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        double2 v;
-        v.x = acc[mi][ni][0];
-        v.y = acc[mi][ni][1];
-        *reinterpret_cast<double2*>(T + sw_off(rr, cbase + ni * 8 + 2 * lc)) = v;
-      }
+      for (int ni = 0; ni < NI; ++ni)
+        *reinterpret_cast<double2*>(T + sw_off(rr, ni * 8 + 2 * lc)) =
+            NEG ? make_double2(-acc[mi][ni][0], -acc[mi][ni][1])
+                : make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     }
 }
 
 template <bool NEG>
 __device__ __forceinline__ void frag_store(const Acc& acc, double* __restrict__ T, int rbase,
-                                           int cbase, int mlim, int lane) {
+                                           int mlim, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
     if (mi < mlim) {
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        double2 v;
-        v.x = NEG ? -acc[mi][ni][0] : acc[mi][ni][0];
-        v.y = NEG ? -acc[mi][ni][1] : acc[mi][ni][1];
-        *reinterpret_cast<double2*>(T + sw_off(rbase + mi * 8 + lr, cbase + ni * 8 + 2 * lc)) = v;
-      }
+      for (int ni = 0; ni < NI; ++ni)
+        *reinterpret_cast<double2*>(T + sw_off(rbase + mi * 8 + lr, ni * 8 + 2 * lc)) =
+            NEG ? make_double2(-acc[mi][ni][0], -acc[mi][ni][1])
+                : make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     }
 }
 
 __device__ __forceinline__ void frag_zero(Acc& acc) {
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 }
 
 struct Pipe {
@@ -323,13 +304,14 @@ struct Src {
 // acc += Σ_q A_q B_qᵀ over nq chunks streamed from global memory:
 //   A rows of tile a: gA0 + q·CHUNK_D (cA0 rows copied), tile b: gA1 (cA1 rows),
 //   B rows: gB (cB rows).
-// There is no CTA-wide barrier per chunk: each warp waits only for its data
-// (full mbarrier) and releases the stage with a non-blocking arrive on its empty
-// mbarrier; at the start of chunk q one warp (rotating) waits for the stage of
-// chunk q−1 to be released and refills it with chunk q−1+NSTAGE.  The caller must
-// __syncthreads() between two k-loops.
+// There is no CTA-wide barrier, per chunk or between k-loops: each warp waits only
+// for its data (full mbarrier) and releases the stage with a non-blocking arrive on
+// its empty mbarrier; every copy into a stage first waits for the release of the
+// stage's previous round (the ring runs on across k-loops: pp.seq counts chunks).
+// At the start of chunk q one warp (rotating) refills the stage of chunk q−1 with
+// chunk q−1+NSTAGE; the first NSTAGE chunks are issued by the lead thread.
 __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
-                                      bool mine_b, int rbase, int mlim, int cbase, int lane,
+                                      bool mine_b, int rbase, int mlim, int lane,
                                       const double* slot_lo, const double* slot_hi) {
   const int tid = threadIdx.x;
   const uint32_t seq = pp.seq;
@@ -359,9 +341,13 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
   // warps of one row block may take different paths.
   auto producer = [&](int q) { return (tid >> 5) == (int)((seq + q) & 7) && (tid & 31) == 0; };
   if (tid == LEAD_TID)
-    for (int q = 0; q < NSTAGE && q < nq; ++q) issue(q);
+    for (int q = 0; q < NSTAGE && q < nq; ++q) {
+      const uint32_t u = seq + q;
+      if (u >= NSTAGE) mbar_wait(saddr(&pp.empty[u % NSTAGE]), (u / NSTAGE - 1) & 1);
+      issue(q);
+    }
 #ifndef LIK_NO_SWP
-  if (mlim == 4) {
+  if (mlim == MI) {
     // Software-pipelined full-tile path: the fragments of k-step t+1 are loaded
     // before the 16 DMMAs of k-step t are issued; the next chunk's first fragments
     // after the stage is released and its full barrier completes.  (Loading them
@@ -369,18 +355,18 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
     // slower.)
     const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
     const int aoff = mine_b ? CHUNK_D : 0;
-    double fa[2][4], fb[2][4];
+    double fa[2][MI], fb[2][NI];
     auto stage_of = [&](int q) { return pp.stages + ((seq + q) % NSTAGE) * STAGE_D; };
     auto wait_full = [&](int q) {
       const uint32_t u = seq + q;
       mbar_wait(saddr(&pp.mbar[u % NSTAGE]), (u / NSTAGE) & 1);
     };
-    auto load = [&](double (&a)[4], double (&b)[4], const double* st, int kk) {
+    auto load = [&](double (&a)[MI], double (&b)[NI], const double* st, int kk) {
       const int kcol = ((kk * 4) ^ sw) + lc;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = st[aoff + (rbase + mi * 8 + lr) * KC + kcol];
+      for (int mi = 0; mi < MI; ++mi) a[mi] = st[aoff + (rbase + mi * 8 + lr) * KC + kcol];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = st[2 * CHUNK_D + (cbase + ni * 8 + lr) * KC + kcol];
+      for (int ni = 0; ni < NI; ++ni) b[ni] = st[2 * CHUNK_D + (ni * 8 + lr) * KC + kcol];
     };
     wait_full(0);
     load(fa[0], fb[0], stage_of(0), 0);
@@ -398,9 +384,9 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
           load(fa[cur ^ 1], fb[cur ^ 1], st, kk + 1);
         }
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], fa[cur][mi], fb[cur][ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], fa[cur][mi], fb[cur][ni]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(saddr(&pp.empty[(seq + q) % NSTAGE]));
@@ -428,7 +414,7 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
     if (tid == 224) atomicAdd(&g_lik_phase[q == 0 ? 9 : 15], (unsigned long long)(clock64() - tw0));
 #endif
     const double* st = pp.stages + s * STAGE_D;
-    mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, cbase, lane);
+    mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(saddr(&pp.empty[s]));
   }
@@ -750,9 +736,9 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
   int* flag = reinterpret_cast<int*>(sm + OFF_MBAR + 2 * NSTAGE);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = w >> 1, wc = w & 1;
-  const int rbase = (wr & 1) * 32, cbase = wc * 32;
-  const bool mine_b = wr >= 2;
+  const int sel = w >> 2;           // the warp's tile row in a row block: 0 → ia, 1 → ib
+  const int rbase = 16 * (w & 3);   // its 16 rows of that tile (all 64 columns)
+  const bool mine_b = sel == 1;
   const int k = A.k0 + blockIdx.x;
   const SlotGeom g = A.g;
   const int nt = g.nt, M = A.M, p = A.p, r = g.r;
@@ -794,6 +780,11 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
 
   Acc acc;
   PH_INIT();
+  // Row blocks run without CTA barriers (each warp solves its own rows from its
+  // registers); the barriers are at a column's first row block (the diagonal tile is
+  // staged in the ring's shared memory and factored by all warps) and at its end
+  // (the proxy fence before the column's L tiles are read through TMA, and L_jj⁻¹
+  // is rewritten by the next column).
   for (int j = 0; j < nt; ++j) {
     const int nrow = MG ? nt - j : nt - j + 1;  // tile rows j..nt-1 (and the augmented row)
     for (int rb = 0; rb < nrow; rb += 2) {
@@ -806,88 +797,83 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
         if (ib >= 0) prefetch_l2(tile_ptr(ib, j), (uint32_t)copy_rows(ib) * TB * 8);
       }
 #endif
-      const int vmine = mine_b ? (ib >= 0 ? valid_rows(ib) : 0) : valid_rows(ia);
-      const int mlim = max(0, min(4, (vmine - rbase + 7) >> 3));
-      // acc = Σ_k L_ik L_jkᵀ, then C = A_ij − acc (stored negated in the staging below)
+      const int ti = sel ? ib : ia;  // −1: this warp has no tile in a single-row block
+      const int vmine = ti >= 0 ? valid_rows(ti) : 0;
+      const int mlim = max(0, min(MI, (vmine - rbase + 7) >> 3));
+      // acc = Σ_k L_ik L_jkᵀ − A_ij = −C
       frag_zero(acc);
       PH(0);
       if (j > 0)
-        kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, cbase, lane, ws,
+        kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, lane, ws,
               ws + g.slot_d);
       PH(1);
-      {
-        const int ti = mine_b ? (ib >= 0 ? ib : ia) : ia;
+      if (ti >= 0) {
         if (is_m(ti))
-          frag_sub_from2(acc, tile_ptr(ti, j), tile_ptr(nt, j), g.off, rbase, cbase, mlim, lane);
+          frag_sub_from2(acc, tile_ptr(ti, j), tile_ptr(nt, j), g.off, rbase, mlim, lane);
         else
-          frag_sub_from(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
+          frag_sub_from(acc, tile_ptr(ti, j), rbase, mlim, lane);
       }
-      __syncthreads();
-      PH(2);
-      frag_store<true>(acc, staging + (mine_b ? TILE_D : 0), rbase, cbase, mlim, lane);
-      __syncthreads();
-      PH(3);
-      if (rb == 0 && is_m(j)) {
-        // merged last diagonal tile: partial factorisation; its Schur block is −BᵀV⁻¹B
-        if (potrf_tail(staging, g.vlast, tol, dlog, flag, Linv)) {
-          write_point_failure(A, k, LIK_PT_V_NOT_PD);
-          return;
-        }
-        if (tid == LEAD_TID) {
-          double s = 0.0;
-          for (int c = 0; c < g.vlast; ++c) s += dlog[c];
-          logdet += s;
-        }
-      } else if (rb == 0) {
-        // diagonal tile: factor, log-determinant, inverse for this column's solves
-        if (potrf_inv64(staging, valid_rows(j), tol, dlog, flag, Linv, sm + OFF_SCRATCH)) {
-          write_point_failure(A, k, LIK_PT_V_NOT_PD);
-          return;
-        }
-        if (tid == LEAD_TID) {
-          double s = 0.0;
-          for (int c = 0; c < valid_rows(j); ++c) s += dlog[c];
-          logdet += s;
-        }
-        PH(4);
+      if (rb == 0) {
+        __syncthreads();  // every warp is past the k-loop: the ring's memory is free
+        PH(2);
+        if (sel == 0) frag_store<true>(acc, staging, rbase, mlim, lane);  // C_jj
         __syncthreads();
-        PH(5);
-        if (ib >= 0 && mine_b) {
-          frag_zero(acc);
-          trsm_any(acc, staging + TILE_D, rbase, mlim, Linv, wc, lane);
-          if (is_m(ib))
-            frag_store2(acc, tile_ptr(ib, j), tile_ptr(nt, j), g.off, rbase, cbase, mlim, lane);
-          else
-            frag_store<false>(acc, tile_ptr(ib, j), rbase, cbase, mlim, lane);
+        PH(3);
+        if (is_m(j)) {
+          // merged last diagonal tile: partial factorisation; its Schur block is −BᵀV⁻¹B
+          if (potrf_tail(staging, g.vlast, tol, dlog, flag, Linv)) {
+            write_point_failure(A, k, LIK_PT_V_NOT_PD);
+            return;
+          }
+          if (tid == LEAD_TID) {
+            double s = 0.0;
+            for (int c = 0; c < g.vlast; ++c) s += dlog[c];
+            logdet += s;
+          }
+        } else {
+          // diagonal tile: factor, log-determinant, inverse for this column's solves
+          if (potrf_inv64(staging, valid_rows(j), tol, dlog, flag, Linv, sm + OFF_SCRATCH)) {
+            write_point_failure(A, k, LIK_PT_V_NOT_PD);
+            return;
+          }
+          if (tid == LEAD_TID) {
+            double s = 0.0;
+            for (int c = 0; c < valid_rows(j); ++c) s += dlog[c];
+            logdet += s;
+          }
+          PH(4);
+          __syncthreads();  // L_jj⁻¹ complete; the ring's memory is free again
+          PH(5);
         }
-      } else {
-        // L_ij = C L_jj⁻ᵀ for both tile rows of the block
-        frag_zero(acc);
-        trsm_any(acc, staging + (mine_b ? TILE_D : 0), rbase, mlim, Linv, wc, lane);
-        const int ti = mine_b ? ib : ia;
-        if (ti >= 0 && is_m(ti))
-          frag_store2(acc, tile_ptr(ti, j), tile_ptr(nt, j), g.off, rbase, cbase, mlim, lane);
-        else if (ti >= 0)
-          frag_store<false>(acc, tile_ptr(ti, j), rbase, cbase, mlim, lane);
+      }
+      // L_ij = C L_jj⁻ᵀ from the warp's registers (acc = −C gives −L_ij)
+      if (ti >= 0 && !(rb == 0 && sel == 0) && mlim > 0) {
+        trsm_reg(acc, Linv, lane);
+        if (is_m(ti))
+          frag_store2<true>(acc, tile_ptr(ti, j), tile_ptr(nt, j), g.off, rbase, mlim, lane);
+        else
+          frag_store<true>(acc, tile_ptr(ti, j), rbase, mlim, lane);
       }
       PH(6);
       // L tiles written in column j are read through TMA only from column j+1 on
       // (and by the final block), so one proxy fence per column suffices.
-      if (rb + 2 >= nrow) fence_proxy_async();
-      __syncthreads();
+      if (rb + 2 >= nrow) {
+        fence_proxy_async();
+        __syncthreads();
+      }
       PH(7);
     }
   }
 
   // ssqYX = BᵀV⁻¹B (Table 1, Step 4)
   if (!MG) {
-    // separate augmented row: acc = Σ_k Z_k Z_kᵀ over its final block
-    const int mlim = mine_b ? 0 : max(0, min(4, (g.Ra - rbase + 7) >> 3));
+    // separate augmented row: acc = Σ_k Z_k Z_kᵀ over its final block (warps 0-3)
+    const int mlim = mine_b ? 0 : max(0, min(MI, (g.Ra - rbase + 7) >> 3));
     frag_zero(acc);
     kloop(acc, pp, src(nt), Src{nullptr, 0, nullptr, 0}, src(nt), CHUNKS * nt, false, rbase, mlim,
-          cbase, lane, ws, ws + g.slot_d);
+          lane, ws, ws + g.slot_d);
     __syncthreads();
-    frag_store<false>(acc, staging, rbase, cbase, mlim, lane);
+    frag_store<false>(acc, staging, rbase, mlim, lane);
     __syncthreads();
   }
   // Steps 5-8 and Eq. (profile)

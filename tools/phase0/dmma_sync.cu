@@ -49,7 +49,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   }
 }
 
-template <int MODE>
+template <int MODE, bool T16 = false>
 __global__ void __launch_bounds__(256, 2) k(double* out, int nq, const double* src) {
   extern __shared__ __align__(128) double sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + NSTAGE * STAGE_D);
@@ -61,16 +61,19 @@ __global__ void __launch_bounds__(256, 2) k(double* out, int nq, const double* s
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int rbase = (wr & 1) * 32, cbase = wc * 32, lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
-  const int aoff = wr >= 2 ? CHUNK_D : 0;
-  double acc[4][4][2] = {};
-  double fa[2][4], fb[2][4];
-  auto load = [&](double (&a)[4], double (&b)[4], const double* st, int kk) {
+  // T16: warp tile 16 rows x 64 columns (full rows); else 32 x 32
+  constexpr int MI = T16 ? 2 : 4, NI = T16 ? 8 : 4;
+  const int rbase = T16 ? 16 * (w & 3) : (wr & 1) * 32, cbase = T16 ? 0 : wc * 32;
+  const int lr = lane >> 2, lc = lane & 3, sw = (lr & 3) << 2;
+  const int aoff = (T16 ? w >= 4 : wr >= 2) ? CHUNK_D : 0;
+  double acc[MI][NI][2] = {};
+  double fa[2][MI], fb[2][NI];
+  auto load = [&](double (&a)[MI], double (&b)[NI], const double* st, int kk) {
     const int kcol = ((kk * 4) ^ sw) + lc;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) a[mi] = st[aoff + (rbase + mi * 8 + lr) * KC + kcol];
+    for (int mi = 0; mi < MI; ++mi) a[mi] = st[aoff + (rbase + mi * 8 + lr) * KC + kcol];
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = st[2 * CHUNK_D + (cbase + ni * 8 + lr) * KC + kcol];
+    for (int ni = 0; ni < NI; ++ni) b[ni] = st[2 * CHUNK_D + (cbase + ni * 8 + lr) * KC + kcol];
   };
   auto lead = [&](int q) { return MODE == 2 ? (q % 8) : 7; };
   // prologue: the "copies" of the first NSTAGE chunks land immediately
@@ -106,9 +109,9 @@ __global__ void __launch_bounds__(256, 2) k(double* out, int nq, const double* s
         const int cur = kk & 1;
         if (kk + 1 < KC / 4) load(fa[cur ^ 1], fb[cur ^ 1], st, kk + 1);
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], fa[cur][mi], fb[cur][ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], fa[cur][mi], fb[cur][ni]);
       }
       if (MODE) {
         __syncwarp();
@@ -123,16 +126,16 @@ __global__ void __launch_bounds__(256, 2) k(double* out, int nq, const double* s
     if (MODE == 4) __syncthreads();
   }
   double s = 0;
-  for (int mi = 0; mi < 4; ++mi)
-    for (int ni = 0; ni < 4; ++ni) s += acc[mi][ni][0] + acc[mi][ni][1];
+  for (int mi = 0; mi < MI; ++mi)
+    for (int ni = 0; ni < NI; ++ni) s += acc[mi][ni][0] + acc[mi][ni][1];
   if (s == 1234.5) out[0] = s;
   // every issued copy is for a chunk < nq, which all warps waited on: none is in flight here
 }
 
-template <int MODE>
+template <int MODE, bool T16 = false>
 void run(int bpsm, double* o) {
   const size_t smem = NSTAGE * STAGE_D * 8 + 64;
-  cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k<MODE, T16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = 148 * bpsm, nq = 20000;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -142,17 +145,17 @@ void run(int bpsm, double* o) {
     cudaMalloc(&src, (size_t)64 * STAGE_D * 8);
     cudaMemset(src, 0, (size_t)64 * STAGE_D * 8);
   }
-  k<MODE><<<grid, 256, smem>>>(o, 100, src);
+  k<MODE, T16><<<grid, 256, smem>>>(o, 100, src);
   cudaDeviceSynchronize();
   cudaEventRecord(a);
-  k<MODE><<<grid, 256, smem>>>(o, nq, src);
+  k<MODE, T16><<<grid, 256, smem>>>(o, nq, src);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   const double flops = (double)grid * 8 * nq * 4 * 16 * 512.0;
-  printf("{\"kind\":\"dmma_sync\",\"mode\":%d,\"ctas_per_sm\":%d,\"tflops\":%.2f,\"err\":\"%s\"}\n", MODE,
-         bpsm, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  printf("{\"kind\":\"dmma_sync\",\"mode\":%d,\"tile\":\"%s\",\"ctas_per_sm\":%d,\"tflops\":%.2f,\"err\":\"%s\"}\n", MODE,
+         T16 ? "16x64" : "32x32", bpsm, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main(int argc, char** argv) {
@@ -164,6 +167,8 @@ int main(int argc, char** argv) {
     run<2>(bpsm, o);
     run<3>(bpsm, o);
     run<4>(bpsm, o);
+    run<0, true>(bpsm, o);
+    run<4, true>(bpsm, o);
   }
   return 0;
 }
