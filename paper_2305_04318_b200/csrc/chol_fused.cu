@@ -7,7 +7,7 @@
 //     C  = A_ij − Σ_{k<j} L_ik L_jkᵀ            (FP64 DMMA.8x8x4 tensor cores)
 //     i = j:  C = L_jj L_jjᵀ (unblocked, shared memory), log|V| += Σ log pivots,
 //             L_jj⁻¹ for the solves of this column
-//     i > j:  L_ij = C L_jj⁻ᵀ                   (DMMA)
+//     i > j:  L_ij = C L_jj⁻ᵀ                   (DMMA, from the warp's registers)
 // The augmented row ends up holding Zᵀ = (L⁻¹B)ᵀ (Step 3), and its final
 // diagonal block  Σ_k Z_k Z_kᵀ = BᵀV⁻¹B  is the cross-product matrix ssqYX of
 // Table 1 (Step 4).  The epilogue does Steps 5-8 and Eq. (profile).
@@ -17,10 +17,12 @@
 // (cp.async.bulk, the TMA engine) completing on an mbarrier; a 3-stage ring.
 // The L_j panel (B operand, reused by every row block of column j) is loaded
 // with an L2 evict_last policy, the streamed A panels with evict_first.
-// 256 threads = 8 warps as 4 (32-row) × 2 (32-column) warp tiles of a 128×64
-// row block; each warp owns 4×4 DMMA 8×8 accumulators.  Two CTAs per SM
-// (≤ 128 registers, ~105 KB shared memory each), so the serial phases of one
-// point (diagonal factorisation, inverse) overlap the DMMA phases of the other.
+// 256 threads = 8 warps; warp w owns 16 full rows (all 64 columns) of tile row
+// w/4 of the 128×64 row block: 2×8 DMMA 8×8 accumulators, so the triangular
+// solve runs from its own registers and row blocks need no CTA barrier.  Two
+// CTAs per SM (≤ 128 registers, ~105 KB shared memory each), so the serial
+// phases of one point (diagonal factorisation, inverse) overlap the DMMA phases
+// of the other.
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
