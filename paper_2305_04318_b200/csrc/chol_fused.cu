@@ -348,59 +348,11 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
       if (u >= NSTAGE) mbar_wait(saddr(&pp.empty[u % NSTAGE]), (u / NSTAGE - 1) & 1);
       issue(q);
     }
-#ifndef LIK_NO_SWP
-  if (mlim == MI) {
-    // Software-pipelined full-tile path: the fragments of k-step t+1 are loaded
-    // before the 16 DMMAs of k-step t are issued; the next chunk's first fragments
-    // after the stage is released and its full barrier completes.  (Loading them
-    // before the last k-step — blocking or with a non-blocking probe — measured
-    // slower.)
-    const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
-    const int aoff = mine_b ? CHUNK_D : 0;
-    double fa[2][MI], fb[2][NI];
-    auto stage_of = [&](int q) { return pp.stages + ((seq + q) % NSTAGE) * STAGE_D; };
-    auto wait_full = [&](int q) {
-      const uint32_t u = seq + q;
-      mbar_wait(saddr(&pp.mbar[u % NSTAGE]), (u / NSTAGE) & 1);
-    };
-    auto load = [&](double (&a)[MI], double (&b)[NI], const double* st, int kk) {
-      const int kcol = ((kk * 4) ^ sw) + lc;
-#pragma unroll
-      for (int mi = 0; mi < MI; ++mi) a[mi] = st[aoff + (rbase + mi * 8 + lr) * KC + kcol];
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) b[ni] = st[2 * CHUNK_D + (ni * 8 + lr) * KC + kcol];
-    };
-    wait_full(0);
-    load(fa[0], fb[0], stage_of(0), 0);
-    for (int q = 0; q < nq; ++q) {
-      if (producer(q) && q >= 1 && q - 1 + NSTAGE < nq) {
-        const uint32_t u = seq + q - 1;
-        mbar_wait(saddr(&pp.empty[u % NSTAGE]), (u / NSTAGE) & 1);
-        issue(q - 1 + NSTAGE);
-      }
-      const double* st = stage_of(q);
-#pragma unroll
-      for (int kk = 0; kk < KC / 4; ++kk) {
-        const int cur = kk & 1;  // KC/4 is even: chunk q+1 starts again in buffer 0
-        if (kk + 1 < KC / 4) {
-          load(fa[cur ^ 1], fb[cur ^ 1], st, kk + 1);
-        }
-#pragma unroll
-        for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], fa[cur][mi], fb[cur][ni]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(saddr(&pp.empty[(seq + q) % NSTAGE]));
-      if (q + 1 < nq) {
-        wait_full(q + 1);
-        load(fa[0], fb[0], stage_of(q + 1), 0);
-      }
-    }
-    pp.seq = seq + nq;
-    return;
-  }
-#endif
+  // (A software-pipelined variant of this loop — next k-step's fragments loaded
+  // before the current DMMAs, double-buffered — gave no speed-up with two CTAs per
+  // SM and, with the full-row warp tiles, produced run-to-run differences at
+  // ~0.1 % of the points; removed.  tests/test_gpu_parity.py checks bitwise
+  // repeatability over several CTA rounds.)
   for (int q = 0; q < nq; ++q) {
     if (producer(q) && q >= 1 && q - 1 + NSTAGE < nq) {
       const uint32_t u = seq + q - 1;
@@ -578,8 +530,8 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     __syncthreads();
   }
   // Lookahead: after the panel product of panel p, the lead warp updates the next
-  // diagonal block (trailing tile 0) and factors it at once, while the other warps
-  // update the rest of the trailing matrix (disjoint tiles).
+  // diagonal block (the first ND trailing tiles) and factors it at once, while the
+  // other warps update the rest of the trailing matrix (disjoint tiles).
   if (warp == LEAD_WARP) factor_block(S, X, 0, PW, tol, dlog, flag);
   SUB(10);
   __syncthreads();
@@ -591,12 +543,13 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     panel_product(S, X, c0);
     __syncthreads();
     const int rt = (TB - c0 - PW) >> 3, ntile = rt * (rt + 1) / 2;
+    constexpr int ND = (PW / 8) * (PW / 8 + 1) / 2;  // trailing tiles of the next diagonal block
     if (warp == LEAD_WARP) {
-      trailing_tile(S, c0, 0);
+      for (int t = 0; t < ND; ++t) trailing_tile(S, c0, t);
       __syncwarp();
       factor_block(S, X, c0 + PW, PW, tol, dlog, flag);
     } else {
-      for (int t = 1 + warp; t < ntile; t += NT / 32 - 1) trailing_tile(S, c0, t);
+      for (int t = ND + warp; t < ntile; t += NT / 32 - 1) trailing_tile(S, c0, t);
     }
     __syncthreads();
     SUB(13);
@@ -863,6 +816,11 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
         fence_proxy_async();
         __syncthreads();
       }
+#ifdef LIK_DEBUG_RB_BARRIER
+      else {
+        __syncthreads();
+      }
+#endif
       PH(7);
     }
   }

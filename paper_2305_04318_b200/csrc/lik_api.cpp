@@ -241,7 +241,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   c->pc_cap = pcb / sizeof(PointConst);
   if ((rc = ensure(c, &c->bt, &c->bt_bytes, (size_t)g.r * g.nt * lik::TB * sizeof(double) + 64)))
     return rc;
-  if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, sizeof(double)));
+  if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));  // Σ log y, d²min, d²max
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)W * lik::TABLE_D * sizeof(double))))
     return rc;
 
@@ -263,12 +263,13 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   CUDA_TRY(c, lik::launch_prep(coords, y, X, lambdas, dperm, n, p, M, g.nt * lik::TB, c->coords_p,
                                c->bt, c->S, st));
+  CUDA_TRY(c, lik::launch_dist_range(c->coords_p, n, c->S + 1, st));
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   for (int w = 0; w < nwaves; ++w) {
     const int k0 = w * W, kw = std::min(W, K - k0);
-    CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, st));
+    CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, c->S + 1, st));
     CUDA_TRY(c, lik::launch_build(c->coords_p, g, c->pc, k0, kw, c->table, c->bt, c->ws, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
@@ -300,7 +301,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     c->stage_ms[LIK_STAGE_PREP] += ms;
-    c->stage_n[LIK_STAGE_PREP] += 1;
+    c->stage_n[LIK_STAGE_PREP] += 2;  // prep + dist_range
     cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
     c->stage_ms[LIK_STAGE_SETUP] += ms;
     c->stage_n[LIK_STAGE_SETUP] += 1;
@@ -534,8 +535,10 @@ int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const doub
   c->pc_cap = pcb / sizeof(PointConst);
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)K * lik::TABLE_D * sizeof(double))))
     return rc;
+  if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));
+  CUDA_TRY(c, lik::launch_dist_range(coords, n, c->S + 1, st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
-  CUDA_TRY(c, lik::launch_table(c->pc, 0, K, c->table, st));
+  CUDA_TRY(c, lik::launch_table(c->pc, 0, K, c->table, c->S + 1, st));
   CUDA_TRY(c, lik::launch_build(coords, g, c->pc, 0, K, c->table, nullptr, c->ws, st));
   CUDA_TRY(c, lik::launch_unpack_V(g, c->pc, K, c->ws, V, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));

@@ -82,6 +82,7 @@ enum { MODE_BESSEL = 0, MODE_GAUSS = 1, MODE_BAD = 2 };
 struct PointConst {
   double cX, sX, sY, cY;   // u/φX = cX hx − sX hy,  v/φY = sY hx + cY hy
   double kappa, sqrt8k;    // κ, √(8κ)
+  double eightk;           // 8κ (s = z² = 8κ d², exact)
   double mu;               // fractional order μ = κ − nl ∈ [−1/2, 1/2)
   double lnpref;           // (1−κ) ln 2 − ln Γ(κ)
   double gam1, gam2;       // Temme constants of μ
@@ -90,20 +91,21 @@ struct PointConst {
   double nugget;           // ν²
   int nl;                  // forward-recurrence steps (κ = μ + nl)
   int mode;                // MODE_*
-  int e_zero;              // ρ ≡ 0 (ln ρ < −750) for z ≥ 2^e_zero (set by table_kernel)
+  int e_zero;              // ρ ≡ 0 (ln ρ < −750) for s = z² ≥ 2^e_zero (set by table_kernel)
+  int olo, ohi;            // table octaves built for this point (its range of s ± 1 octave)
 };
 
-// Per-point Chebyshev table of ln ρ(z) on binary octaves z ∈ [2^e, 2^{e+1}),
-// e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1.  Each octave stores CHEB_STRIDE
-// doubles: a base H_o, one pad (so the coefficients are 16-byte aligned), then the
-// CHEB_N monomial coefficients (in
-// t = z/2^e·2 − 3 ∈ [−1, 1)) of the degree-19 Chebyshev interpolant of
-// h(z) = ln ρ(z) + z − H_o, so that ln ρ = (H_o + h(z)) − z.  Below 2^CHEB_ELO
-// the exact evaluation is used; at and above 2^e_zero ρ = 0.
+// Per-point Chebyshev table of ln ρ on binary octaves of s = z² = 8κ·d² ∈ [2^e,
+// 2^{e+1}), e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1 (the build needs no square
+// root).  Each octave stores CHEB_STRIDE doubles: a base H_o, one pad (so the
+// coefficients are 16-byte aligned), then the CHEB_N monomial coefficients (in
+// t = s/2^e·2 − 3 ∈ [−1, 1)) of the degree-19 Chebyshev interpolant of
+// h(s) = ln ρ(√s) − H_o, so that ln ρ = H_o + h(s).  Below 2^CHEB_ELO the exact
+// evaluation is used; at and above 2^e_zero ρ = 0.
 constexpr int CHEB_N = 20;
 constexpr int CHEB_STRIDE = CHEB_N + 2;
-constexpr int CHEB_ELO = -26;
-constexpr int CHEB_NOCT = 40;
+constexpr int CHEB_ELO = -52;
+constexpr int CHEB_NOCT = 80;
 constexpr int TABLE_D = CHEB_STRIDE * CHEB_NOCT;
 
 // Launch wrappers (defined in the .cu files).  All enqueue on `st`.
@@ -113,7 +115,11 @@ cudaError_t launch_prep(const double* coords, const double* y, const double* X,
                         const double* lambdas, const int* perm, int n, int p, int M, int npad,
                         double* coords_p, double* Bt, double* S, cudaStream_t st);
 cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st);
-cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, cudaStream_t st);
+// dist_range: dstat[0] = min, dstat[1] = max squared Euclidean distance over the
+// site pairs (one block; bounds each point's range of s = z² for the table).
+cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st);
+cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, const double* dstat,
+                         cudaStream_t st);
 cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
                          int kw, const double* table, const double* Bt, double* ws,
                          cudaStream_t st);

@@ -90,6 +90,7 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
   P.cY = c / phiY;
   P.kappa = kappa;
   P.sqrt8k = sqrt(8.0 * kappa);
+  P.eightk = 8.0 * kappa;
   P.nugget = nug;
   int nl = 0;
   double mu = 0.0;
@@ -100,6 +101,8 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
   P.nl = nl;
   P.mu = mu;
   P.e_zero = 1 << 20;  // set by table_kernel
+  P.olo = 0;
+  P.ohi = CHEB_NOCT - 1;
   P.lnpref = ok && P.mode == MODE_BESSEL ? (1.0 - kappa) * 0.69314718055994530942 - lgamma(kappa) : 0.0;
   temme_constants(mu, &P.gam1, &P.gam2, &P.gampl, &P.gammi, &P.fact);
   pc[k] = P;
@@ -111,15 +114,59 @@ cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream
 }
 
 // ---------------------------------------------------------------------------
+// dist_range: one block; min / max squared Euclidean distance over all site pairs
+// (fixed-order reduction).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) dist_range_kernel(const double* __restrict__ coords, int n,
+                                                         double* __restrict__ dstat) {
+  __shared__ double lo[512], hi[512];
+  double mn = INFINITY, mx = 0.0;
+  const long long np = (long long)n * (n - 1) / 2;
+  for (long long e = threadIdx.x; e < np; e += 512) {
+    // pair e → (i, j), i > j
+    int i = (int)((sqrt(8.0 * (double)e + 1.0) + 1.0) * 0.5);
+    while ((long long)i * (i - 1) / 2 > e) --i;
+    while ((long long)(i + 1) * i / 2 <= e) ++i;
+    const int j = (int)(e - (long long)i * (i - 1) / 2);
+    const double dx = coords[2 * i] - coords[2 * j], dy = coords[2 * i + 1] - coords[2 * j + 1];
+    const double d2 = dx * dx + dy * dy;
+    mn = fmin(mn, d2);
+    mx = fmax(mx, d2);
+  }
+  lo[threadIdx.x] = mn;
+  hi[threadIdx.x] = mx;
+  __syncthreads();
+  for (int w = 256; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      lo[threadIdx.x] = fmin(lo[threadIdx.x], lo[threadIdx.x + w]);
+      hi[threadIdx.x] = fmax(hi[threadIdx.x], hi[threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    dstat[0] = lo[0];
+    dstat[1] = hi[0];
+  }
+}
+
+cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st) {
+  dist_range_kernel<<<1, 512, 0, st>>>(coords, n, dstat);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // table: one block per point of the wave.  ln ρ is evaluated exactly (Temme /
-// CF2 + recurrence) at CHEB_N Chebyshev nodes of every binary octave of z below
-// the underflow octave e_zero, and turned into Chebyshev coefficients (DCT-II).
-// ln ρ(z) is analytic on each octave [a, 2a] (its only finite singularity is the
-// branch point z = 0, three half-widths from the centre), so degree 19 reaches
-// the FP64 rounding floor (~1e-16·max(1, |ln ρ|)), DESIGN.md §5.
+// CF2 + recurrence) at the octave edges and at CHEB_N Chebyshev nodes of every
+// binary octave of s = z² below the underflow octave e_zero, detrended by the line
+// through the edge values (so the DCT works on a small function) and turned into
+// Chebyshev coefficients (DCT-II), then monomial ones with the line added back.
+// ln ρ(√s) is analytic on each octave [a, 2a] (its only finite singularity is the
+// branch point s = 0, three half-widths from the centre), so degree 19 reaches the
+// FP64 rounding floor (~1e-16·max(1, |ln ρ|)), DESIGN.md §5.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc, int k0,
-                                                    double* __restrict__ table) {
+                                                    double* __restrict__ table,
+                                                    const double* __restrict__ dstat) {
   const int k = k0 + blockIdx.x;
   const int tid = threadIdx.x;
   const PointConst P = pc[k];
@@ -127,35 +174,45 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   __shared__ double f[CHEB_NOCT * CHEB_N];
   __shared__ double edge[CHEB_NOCT + 1];
   __shared__ int ez;
-  for (int o = tid; o <= CHEB_NOCT; o += 256) edge[o] = log_rho_exact(P, ldexp(1.0, CHEB_ELO + o));
+  // This point's s = 8κ·|Q h|² lies in [8κ·d²min/φ²max, 8κ·d²max/φ²min] (the singular
+  // values of the anisotropy map Q are 1/φX, 1/φY): only those octaves, widened by
+  // one on each side against rounding, are built; the build sends anything outside
+  // [olo, ohi] to the exact evaluation.
+  const double q_lo = fmin(P.cX * P.cX + P.sX * P.sX, P.sY * P.sY + P.cY * P.cY);
+  const double q_hi = fmax(P.cX * P.cX + P.sX * P.sX, P.sY * P.sY + P.cY * P.cY);
+  const double s_lo = P.eightk * dstat[0] * q_lo, s_hi = P.eightk * dstat[1] * q_hi;
+  const int olo = s_lo > 0.0 ? max(0, min(CHEB_NOCT - 1, ilogb(s_lo) - CHEB_ELO - 1)) : 0;
+  const int ohi = s_hi > 0.0 ? max(olo, min(CHEB_NOCT - 1, ilogb(s_hi) - CHEB_ELO + 1)) : olo;
+  for (int o = olo + tid; o <= ohi + 1; o += 256) edge[o] = log_rho_exact(P, sqrt(ldexp(1.0, CHEB_ELO + o)));
   __syncthreads();
   if (tid == 0) {
     int e0 = CHEB_ELO + CHEB_NOCT + 64;  // sentinel: never underflows inside the table range
-    for (int o = 0; o <= CHEB_NOCT; ++o)
+    for (int o = olo; o <= ohi + 1; ++o)
       if (edge[o] < -750.0) {
         e0 = CHEB_ELO + o;
         break;
       }
     ez = e0;
     pc[k].e_zero = e0;
+    pc[k].olo = olo;
+    pc[k].ohi = ohi;
   }
   __syncthreads();
-  // g(z) = ln ρ(z) + z at the nodes (the −z trend of ln ρ removed)
-  for (int idx = tid; idx < CHEB_NOCT * CHEB_N; idx += 256) {
+  // g = ln ρ(√s) − L_o(x) at the nodes, L_o the line through the octave's edge values
+  for (int idx = olo * CHEB_N + tid; idx < (ohi + 1) * CHEB_N; idx += 256) {
     const int o = idx / CHEB_N, i = idx % CHEB_N;
     const int e = CHEB_ELO + o;
     double v = 0.0;
     if (e < ez) {
       const double x = cospi((i + 0.5) / CHEB_N);
-      const double z = ldexp(1.5 + 0.5 * x, e);
-      v = log_rho_exact(P, z) + z;
+      const double sn = ldexp(1.5 + 0.5 * x, e);
+      v = log_rho_exact(P, sqrt(sn)) - 0.5 * (edge[o] + edge[o + 1]) - 0.5 * (edge[o + 1] - edge[o]) * x;
     }
     f[idx] = v;
   }
   __syncthreads();
-  // per octave: base H_o = g at the middle node; Chebyshev coefficients of g − H_o
-  // (DCT-II), then converted to monomial coefficients in t (T_j has integer
-  // coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
+  // Chebyshev coefficients of g (DCT-II), then monomial coefficients in t (T_j has
+  // integer coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
   __shared__ double cheb[CHEB_NOCT * CHEB_N];
   __shared__ double tco[CHEB_N * CHEB_N];  // tco[j][k] = coefficient of t^k in T_j
   if (tid == 0) {
@@ -167,34 +224,35 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
         tco[jj * CHEB_N + kk] = (kk > 0 ? 2.0 * tco[(jj - 1) * CHEB_N + kk - 1] : 0.0) -
                                 tco[(jj - 2) * CHEB_N + kk];
   }
-  for (int idx = tid; idx < CHEB_NOCT * CHEB_N; idx += 256) {
+  for (int idx = olo * CHEB_N + tid; idx < (ohi + 1) * CHEB_N; idx += 256) {
     const int o = idx / CHEB_N, jj = idx % CHEB_N;
     double cc = 0.0;
     if (CHEB_ELO + o < ez) {
-      const double H = f[o * CHEB_N + CHEB_N / 2];
-      for (int ii = 0; ii < CHEB_N; ++ii) cc += (f[o * CHEB_N + ii] - H) * cospi(jj * (ii + 0.5) / CHEB_N);
+      for (int ii = 0; ii < CHEB_N; ++ii) cc += f[o * CHEB_N + ii] * cospi(jj * (ii + 0.5) / CHEB_N);
       cc *= (jj == 0 ? 1.0 : 2.0) / CHEB_N;
     }
     cheb[idx] = cc;
   }
   __syncthreads();
   double* T = table + (size_t)blockIdx.x * TABLE_D;
-  for (int idx = tid; idx < CHEB_NOCT * CHEB_STRIDE; idx += 256) {
+  for (int idx = olo * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_STRIDE; idx += 256) {
     const int o = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 2;
     double a = 0.0;
     if (CHEB_ELO + o < ez) {
       if (kk == -2) {
-        a = f[o * CHEB_N + CHEB_N / 2];  // H_o
+        a = 0.5 * (edge[o] + edge[o + 1]);  // H_o: the line's value at t = 0
       } else if (kk >= 0) {
         for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[o * CHEB_N + jj] * tco[jj * CHEB_N + kk];
+        if (kk == 1) a += 0.5 * (edge[o + 1] - edge[o]);  // the line's slope in t
       }
     }
     T[idx] = a;
   }
 }
 
-cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, cudaStream_t st) {
-  table_kernel<<<kw, 256, 0, st>>>(pc, k0, table);
+cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, const double* dstat,
+                         cudaStream_t st) {
+  table_kernel<<<kw, 256, 0, st>>>(pc, k0, table, dstat);
   return cudaGetLastError();
 }
 
@@ -225,8 +283,8 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
   if (threadIdx.x < 32) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
   if (P.mode == MODE_BESSEL) {
     const double* src = table + (size_t)slot * TABLE_D;
-    const int nval = min(CHEB_NOCT, max(0, P.e_zero - CHEB_ELO)) * CHEB_STRIDE;
-    for (int e = threadIdx.x; e < nval; e += 256) coef[e] = src[e];
+    const int oend = min(P.ohi + 1, max(P.olo, P.e_zero - CHEB_ELO));  // octaves [olo, oend)
+    for (int e = P.olo * CHEB_STRIDE + threadIdx.x; e < oend * CHEB_STRIDE; e += 256) coef[e] = src[e];
   }
   // thread -> column c, rows r0 + 4q (q < 16): a warp covers 32 consecutive
   // columns of one row; with Morton-ordered sites their z values mostly share an
