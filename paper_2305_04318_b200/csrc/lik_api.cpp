@@ -301,7 +301,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     c->stage_ms[LIK_STAGE_PREP] += ms;
-    c->stage_n[LIK_STAGE_PREP] += 2;  // prep + dist_range
+    c->stage_n[LIK_STAGE_PREP] += 3;  // prep, dist_init, dist_range
     cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
     c->stage_ms[LIK_STAGE_SETUP] += ms;
     c->stage_n[LIK_STAGE_SETUP] += 1;

@@ -116,7 +116,7 @@ cudaError_t launch_prep(const double* coords, const double* y, const double* X,
                         double* coords_p, double* Bt, double* S, cudaStream_t st);
 cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st);
 // dist_range: dstat[0] = min, dstat[1] = max squared Euclidean distance over the
-// site pairs (one block; bounds each point's range of s = z² for the table).
+// site pairs (bounds each point's range of s = z² for the table).
 cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st);
 cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, const double* dstat,
                          cudaStream_t st);

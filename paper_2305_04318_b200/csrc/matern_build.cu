@@ -3,6 +3,7 @@
 //   prep_kernel   — a1: y'_m = b(y; λ_m) (R14), Bᵀ rows, S = Σ log y
 //   setup_kernel  — per-point constants of ω_k (R1, R3, R7)
 //   build_kernel  — a2 "matern_build": V = R + ν²I tiles (P:86, P:311 Step 1)
+#include <algorithm>
 #include <cfloat>
 #include "bessel_k.cuh"
 #include "lik_internal.cuh"
@@ -114,16 +115,23 @@ cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream
 }
 
 // ---------------------------------------------------------------------------
-// dist_range: one block; min / max squared Euclidean distance over all site pairs
-// (fixed-order reduction).
+// dist_range: min / max squared Euclidean distance over all site pairs.  Blocks
+// reduce their share of the pairs and combine with 64-bit integer atomics on the
+// IEEE bit patterns (for non-negative doubles they order like the values), so the
+// result is exact and independent of the order.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) dist_range_kernel(const double* __restrict__ coords, int n,
+__global__ void dist_init_kernel(double* __restrict__ dstat) {
+  dstat[0] = INFINITY;
+  dstat[1] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) dist_range_kernel(const double* __restrict__ coords, int n,
                                                          double* __restrict__ dstat) {
-  __shared__ double lo[512], hi[512];
+  __shared__ double lo[256], hi[256];
   double mn = INFINITY, mx = 0.0;
   const long long np = (long long)n * (n - 1) / 2;
-  for (long long e = threadIdx.x; e < np; e += 512) {
-    // pair e → (i, j), i > j
+  for (long long e = (long long)blockIdx.x * 256 + threadIdx.x; e < np; e += (long long)gridDim.x * 256) {
+    // pair e → (i, j), i > j, e = i(i−1)/2 + j
     int i = (int)((sqrt(8.0 * (double)e + 1.0) + 1.0) * 0.5);
     while ((long long)i * (i - 1) / 2 > e) --i;
     while ((long long)(i + 1) * i / 2 <= e) ++i;
@@ -136,7 +144,7 @@ __global__ void __launch_bounds__(512) dist_range_kernel(const double* __restric
   lo[threadIdx.x] = mn;
   hi[threadIdx.x] = mx;
   __syncthreads();
-  for (int w = 256; w > 0; w >>= 1) {
+  for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w) {
       lo[threadIdx.x] = fmin(lo[threadIdx.x], lo[threadIdx.x + w]);
       hi[threadIdx.x] = fmax(hi[threadIdx.x], hi[threadIdx.x + w]);
@@ -144,13 +152,16 @@ __global__ void __launch_bounds__(512) dist_range_kernel(const double* __restric
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    dstat[0] = lo[0];
-    dstat[1] = hi[0];
+    atomicMin(reinterpret_cast<long long*>(&dstat[0]), __double_as_longlong(lo[0]));
+    atomicMax(reinterpret_cast<long long*>(&dstat[1]), __double_as_longlong(hi[0]));
   }
 }
 
 cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st) {
-  dist_range_kernel<<<1, 512, 0, st>>>(coords, n, dstat);
+  dist_init_kernel<<<1, 1, 0, st>>>(dstat);
+  const long long np = (long long)n * (n - 1) / 2;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(1184, (np + 256 * 64 - 1) / (256 * 64)));
+  dist_range_kernel<<<blocks, 256, 0, st>>>(coords, n, dstat);
   return cudaGetLastError();
 }
 
