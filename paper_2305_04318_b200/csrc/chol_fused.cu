@@ -40,6 +40,20 @@ __device__ unsigned long long g_lik_phase[16];
 #define PH_FLUSH() do {} while (0)
 #endif
 
+#ifdef LIK_CTA_TRACE
+// debug: per-CTA start / end (%globaltimer, ns) and SM id of the last launch
+__device__ unsigned long long g_lik_cta_trace[1 << 16][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#endif
 namespace lik {
 namespace {
 
@@ -682,6 +696,9 @@ __device__ void write_point_failure(const CholArgs& A, int k, int code) {
 #endif
 __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs A) {
   extern __shared__ __align__(1024) double sm[];
+#ifdef LIK_CTA_TRACE
+  const unsigned long long t_start = gtimer();
+#endif
   double* staging = sm;  // aliases the stage ring (used only between k-loops)
   double* Linv = sm + OFF_LINV;
   double* dlog = sm + OFF_DLOG;
@@ -936,12 +953,26 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
   }
   PH(8);
   PH_FLUSH();
+#ifdef LIK_CTA_TRACE
+  if (tid == 0 && blockIdx.x < (1 << 16)) {
+    g_lik_cta_trace[blockIdx.x][0] = t_start;
+    g_lik_cta_trace[blockIdx.x][1] = gtimer();
+    g_lik_cta_trace[blockIdx.x][2] = smid();
+  }
+#endif
 }
 
 }  // namespace
 
 size_t chol_smem_bytes() { return (size_t)SMEM_D * sizeof(double); }
 
+#ifdef LIK_CTA_TRACE
+extern "C" int lik_debug_cta_trace(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_lik_cta_trace, sizeof(unsigned long long) * 3 * (size_t)n);
+  return 0;
+}
+#endif
 #ifdef LIK_PHASE_TIMERS
 extern "C" int lik_debug_phase_cycles(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
