@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
   const int npad = g.nt * TB;
   __shared__ double sx[2][TB], sy[2][TB];
   __shared__ __align__(16) double coef[TABLE_D];
-  __shared__ double etab[32];
-  if (threadIdx.x < 32) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __shared__ double etab[16];
+  if (threadIdx.x < 16) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
   if (P.mode == MODE_BESSEL) {
     const double* src = table + (size_t)slot * TABLE_D;
     const int oend = min(P.ohi + 1, max(P.olo, P.e_zero - CHEB_ELO));  // octaves [olo, oend)
