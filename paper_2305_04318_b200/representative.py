@@ -137,14 +137,15 @@ def _sphere_points(dim: int, n: int, seed: int, iters: int) -> np.ndarray:
     # characteristic spacing of n points on the sphere
     step = 0.5 * (2.0 * math.pi ** (dim / 2) / math.gamma(dim / 2) / n) ** (1.0 / (dim - 1))
     best, best_d = x.copy(), 0.0
+    eye = np.eye(n) * 1e9
     for it in range(iters):
-        diff = x[:, None, :] - x[None, :, :]
-        d2 = (diff * diff).sum(-1) + np.eye(n) * 1e9
+        # on the unit sphere |x_i − x_j|² = 2 − 2 x_i·x_j (Gram matrix: O(n²) memory, not O(n²d))
+        d2 = np.maximum(2.0 - 2.0 * (x @ x.T), 1e-300) + eye
         dmin = math.sqrt(d2.min())
         if dmin > best_d:
             best, best_d = x.copy(), dmin
-        w = 1.0 / d2 ** ((dim + 1) / 2)           # short-range repulsion
-        force = (diff * w[:, :, None]).sum(1)
+        w = d2 ** (-(dim + 1) / 2)                 # short-range repulsion
+        force = x * w.sum(1, keepdims=True) - w @ x   # Σ_j w_ij (x_i − x_j)
         force -= (force * x).sum(1, keepdims=True) * x   # tangential part
         fn = np.linalg.norm(force, axis=1, keepdims=True)
         x = x + step * (1.0 - it / iters) * force / np.maximum(fn, 1e-300)
