@@ -229,11 +229,14 @@ class RepresentativeSet:
 
 
 def configure_params(ctx, coords, y, X, fits, alphas=DEFAULT_ALPHAS, n5: int = 726, n4: int = 120,
-                     m_lambda: int = 33, seed: int = 0, rel_step: float = 1e-3) -> RepresentativeSet:
+                     m_lambda: int = 33, seed: int = 0, rel_step: float = 1e-3,
+                     alphas_fixed=None) -> RepresentativeSet:
     """The paper's configParams: for each fit, a batched stencil evaluation
     of ℓ_p (one lik_eval_batch call, λ ∈ {λ̂ − δ, λ̂, λ̂ + δ}), the Hessian in internal
     coordinates, eigen-repair, contour points at each α, nugget repair; plus the
-    MLEs themselves and the λ grid of the first fit."""
+    MLEs themselves and the λ grid of the first fit.  `alphas_fixed`: the contour
+    levels of the κ-fixed fits (default `alphas`; the paper's examples use 11 resp.
+    10 of their 12 levels there, R26)."""
     rng = np.random.default_rng(seed)
     out_p, out_a, out_s, negHs = [], [], [], []
     curv0 = None
@@ -257,7 +260,8 @@ def configure_params(ctx, coords, y, X, fits, alphas=DEFAULT_ALPHAS, n5: int = 7
             curv0 = curv
         negHs.append(negH)
         sph = sphere_points(len(w0), n5 if len(w0) == 5 else n4, seed=seed)
-        cp, al = contour_points(w0, negH, alphas, sph)
+        levels = alphas if (fit.kappa_fixed is None or alphas_fixed is None) else alphas_fixed
+        cp, al = contour_points(w0, negH, levels, sph)
         nu_col = 2 if fit.kappa_fixed is None else 1
         nug = repair_nugget(cp[:, nu_col], rng)
         cp[:, nu_col] = np.sqrt(nug)

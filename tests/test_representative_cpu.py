@@ -246,3 +246,15 @@ def test_profile_2d_concave_surface():
     exact = -(q[:, 0] ** 2) - 2 * q[:, 1] ** 2 + 0.5 * q[:, 0] * q[:, 1]
     np.testing.assert_allclose(rp.profile_2d(A, B, L, q), exact, atol=0.05)
     assert np.isnan(rp.profile_2d(A, B, L, np.array([[5.0, 5.0]]))[0])
+
+
+def test_configure_params_paper_shapes():
+    """The paper's point counts (R26): Swiss 15,318 = 6 + 12·726 + 5·11·120 (P:582);
+    soil 12,316 = 4 + 12·726 + 3·10·120."""
+    nat0 = np.array([800.0, 1.2, 0.5, 2.0, 0.3])
+    regime = rp.kappa_regime(nat0[1])
+    ctx = QuadraticCtx(np.eye(5), rp.to_internal(nat0, regime)[0], regime)
+    for kfix, nlev, total in (((0.5, 0.9, 10.0, 20.0, 100.0), 11, 15318), ((0.5, 0.8, 1.0), 10, 12316)):
+        fits = [rp.Fit(nat0, 0.3)] + [rp.Fit(np.r_[nat0[0], k, nat0[2:]], 0.3, kappa_fixed=k) for k in kfix]
+        rs = rp.configure_params(ctx, None, None, None, fits, alphas_fixed=rp.DEFAULT_ALPHAS[12 - nlev:])
+        assert rs.params.shape == (total, 5)

@@ -50,12 +50,16 @@ for name, n, p, K, M in (("swiss", 100, 2, 15318, 34), ("soil", 829, 18, 12316, 
     F = n ** 3 / 3 + n * n * r + n * r * r
     # Step 2: 6 fits (κ free + the 5 κ-fixed of P:582), stencil Hessians on the
     # GPU (51·3 / 33·3 likelihoods each), 726 / 120 sphere points × 12 α, λ grid of M−1 + λ̂
+    # the paper's shapes (R26): Swiss — κ free + fixed at 0.5, 0.9, 10, 20, 100, the fixed fits
+    # on 11 of the 12 levels (15,318 points); soil — κ free + fixed at 0.5, 0.8, 1 on
+    # 10 levels (12,316 points)
     nat = np.array(P[0]); nat[1] = 2.0
-    fits = [rp.Fit(nat, 0.5)] + [rp.Fit(np.r_[nat[0], kf, nat[2:]], 0.5, kappa_fixed=kf)
-                                 for kf in synthgen.KAPPA_FIXED]
+    kfix, nlev = ((0.5, 0.9, 10.0, 20.0, 100.0), 11) if name == "swiss" else ((0.5, 0.8, 1.0), 10)
+    fits = [rp.Fit(nat, 0.5)] + [rp.Fit(np.r_[nat[0], kf, nat[2:]], 0.5, kappa_fixed=kf) for kf in kfix]
+    afix = rp.DEFAULT_ALPHAS[len(rp.DEFAULT_ALPHAS) - nlev:]
     import time
-    t0 = time.perf_counter(); rs = rp.configure_params(ctx, coords, y, X, fits, m_lambda=M - 1)
-    t1 = time.perf_counter(); rs = rp.configure_params(ctx, coords, y, X, fits, m_lambda=M - 1)
+    t0 = time.perf_counter(); rs = rp.configure_params(ctx, coords, y, X, fits, m_lambda=M - 1, alphas_fixed=afix)
+    t1 = time.perf_counter(); rs = rp.configure_params(ctx, coords, y, X, fits, m_lambda=M - 1, alphas_fixed=afix)
     t2 = time.perf_counter()
     print(json.dumps({"workload": name, "n": n, "p": p, "K": K, "M": M,
                       "eval_ms": round(ev_ms, 3), "points_per_s": K / (ev_ms / 1e3),
