@@ -5,12 +5,17 @@
 //   for tile column j:   for row blocks (two tile rows at a time, i ≥ j, then the
 //   augmented row):
 //     C  = A_ij − Σ_{k<j} L_ik L_jkᵀ            (FP64 DMMA.8x8x4 tensor cores)
-//     i = j:  C = L_jj L_jjᵀ (unblocked, shared memory), log|V| += Σ log pivots,
-//             L_jj⁻¹ for the solves of this column
+//     i = j:  C = L_jj L_jjᵀ in shared memory: 8-column panels, the 8×8 diagonal
+//             blocks factored and inverted in registers by the lead warp, panel
+//             products / trailing updates / the block-recursive L_jj⁻¹ on DMMA,
+//             with lookahead; log|V| += Σ log pivots
 //     i > j:  L_ij = C L_jj⁻ᵀ                   (DMMA, from the warp's registers)
 // The augmented row ends up holding Zᵀ = (L⁻¹B)ᵀ (Step 3), and its final
 // diagonal block  Σ_k Z_k Z_kᵀ = BᵀV⁻¹B  is the cross-product matrix ssqYX of
-// Table 1 (Step 4).  The epilogue does Steps 5-8 and Eq. (profile).
+// Table 1 (Step 4).  When the B rows fit in the padding of the last
+// diagonal tile ("merged tail"), they ride in that tile instead, and its partial
+// factorisation leaves −BᵀV⁻¹B as the Schur block.  The epilogue does Steps 5-8
+// and Eq. (profile).
 //
 // Operand staging: tiles are stored as contiguous 64×16 swizzled chunks
 // (lik_internal.cuh), so each pipeline stage is three 1-D bulk copies
