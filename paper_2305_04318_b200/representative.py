@@ -226,34 +226,43 @@ class RepresentativeSet:
     source: np.ndarray                  # K: index of the fit each point came from
     neg_hessians: list = field(default_factory=list)
     lambda_curvature: float = float("nan")
+    stencil_loglik: list = field(default_factory=list)  # per fit: stencil points × (λ̂−δ, λ̂, λ̂+δ)
 
 
 def configure_params(ctx, coords, y, X, fits, alphas=DEFAULT_ALPHAS, n5: int = 726, n4: int = 120,
                      m_lambda: int = 33, seed: int = 0, rel_step: float = 1e-3,
                      alphas_fixed=None) -> RepresentativeSet:
-    """The paper's configParams: for each fit, a batched stencil evaluation
-    of ℓ_p (one lik_eval_batch call, λ ∈ {λ̂ − δ, λ̂, λ̂ + δ}), the Hessian in internal
+    """The paper's configParams: the stencil likelihoods of all fits in one
+    batched lik_eval_batch call (each fit's λ̂ − δ, λ̂, λ̂ + δ), then per fit the Hessian in internal
     coordinates, eigen-repair, contour points at each α, nugget repair; plus the
     MLEs themselves and the λ grid of the first fit.  `alphas_fixed`: the contour
     levels of the κ-fixed fits (default `alphas`; the paper's examples use 11 resp.
     10 of their 12 levels there, R26)."""
     rng = np.random.default_rng(seed)
-    out_p, out_a, out_s, negHs = [], [], [], []
-    curv0 = None
-    for f_i, fit in enumerate(fits):
+    # all fits' stencils in ONE batched call: the dataset is shared, and the λ columns
+    # are the union of every fit's {λ̂ − δ, λ̂, λ̂ + δ} (each stencil reads its own three)
+    setup = []
+    for fit in fits:
         regime = kappa_regime(float(fit.natural[1]))
         w0 = to_internal(fit.natural, regime)[0]
         if fit.kappa_fixed is not None:
             w0 = np.delete(w0, 1)
         delta = rel_step * np.maximum(1.0, np.abs(w0))
-        pts = stencil(w0, delta)
-        nat = to_natural(pts, regime, fit.kappa_fixed)
         dl = rel_step * max(1.0, abs(fit.lambda_hat))
-        lam3 = np.array([fit.lambda_hat - dl, fit.lambda_hat, fit.lambda_hat + dl])
-        res = ctx.eval_batch(coords, y, X, nat, lam3)
-        if not np.all(res["status"] == 0):
-            raise RuntimeError(f"fit {f_i}: stencil point with status {res['status']}")
-        ll = res["loglik"]
+        setup.append((regime, w0, delta, dl, to_natural(stencil(w0, delta), regime, fit.kappa_fixed)))
+    lam_all = np.concatenate([[f.lambda_hat - su[3], f.lambda_hat, f.lambda_hat + su[3]]
+                              for f, su in zip(fits, setup)])
+    res = ctx.eval_batch(coords, y, X, np.concatenate([su[4] for su in setup]), lam_all)
+    out_p, out_a, out_s, negHs, stencil_ll = [], [], [], [], []
+    curv0 = None
+    row = 0
+    for f_i, (fit, (regime, w0, delta, dl, nat)) in enumerate(zip(fits, setup)):
+        rows = slice(row, row + len(nat))
+        row += len(nat)
+        if not np.all(res["status"][rows] == 0):
+            raise RuntimeError(f"fit {f_i}: stencil point with status {res['status'][rows]}")
+        ll = res["loglik"][rows, 3 * f_i:3 * f_i + 3]
+        stencil_ll.append(ll)
         negH = -hessian_from_stencil(ll[:, 1], delta)
         curv = (ll[0, 2] - 2 * ll[0, 1] + ll[0, 0]) / dl ** 2
         if curv0 is None:
@@ -274,7 +283,7 @@ def configure_params(ctx, coords, y, X, fits, alphas=DEFAULT_ALPHAS, n5: int = 7
     out_a.append(np.full(len(fits), np.nan))
     out_s.append(np.arange(len(fits)))
     return RepresentativeSet(np.concatenate(out_p), lambda_grid(fits[0].lambda_hat, curv0, m_lambda),
-                             np.concatenate(out_a), np.concatenate(out_s), negHs, curv0)
+                             np.concatenate(out_a), np.concatenate(out_s), negHs, curv0, stencil_ll)
 
 
 # --------------------------------------------------------------------------- profiles (NEXT-4)

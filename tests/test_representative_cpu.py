@@ -177,7 +177,7 @@ def test_configure_params_recovers_the_hessian_and_counts():
     ctx = QuadraticCtx(A, w0, regime)
     fits = [rp.Fit(nat0, 0.3), rp.Fit(nat0, 0.3, kappa_fixed=1.2)]
     rs = rp.configure_params(ctx, None, None, None, fits, n5=40, n4=20, m_lambda=7)
-    assert ctx.calls == 2
+    assert ctx.calls == 1  # all stencils in one batched call
     np.testing.assert_allclose(rs.neg_hessians[0], A, rtol=1e-5, atol=1e-5 * np.abs(A).max())
     A4 = np.delete(np.delete(A, 1, 0), 1, 1)
     np.testing.assert_allclose(rs.neg_hessians[1], A4, rtol=1e-5, atol=1e-5 * np.abs(A).max())
