@@ -106,6 +106,30 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def slot_bytes(n: int, r: int) -> int:
+    """Workspace bytes the build writes per point: the lower tile triangle of V plus one
+    row of augmented tiles, 64×64 FP64 each (lik_internal.cuh SlotGeom)."""
+    nt = (n + 63) // 64
+    return (nt * (nt + 1) // 2 + nt) * 64 * 64 * 8
+
+
+def hbm_peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except Exception:
+        return None
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(coords, y, X, P, lam, budget_s=20.0):
     """The oracle, as it stands, on the host cores over a bounded sample of points."""
     import oracle
@@ -122,7 +146,7 @@ def cpu_baseline(coords, y, X, P, lam, budget_s=20.0):
         oracle.eval_batch(coords, y, X, P[T:T * rounds], lam, nthreads=T)
         tt += time.perf_counter() - t0
         npts += T * (rounds - 1)
-    return {"value": npts / tt, "unit": UNIT, "cores": T, "kind": "oracle",
+    return {"value": npts / tt, "unit": UNIT, "cores": T, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{npts} points of {WORKLOAD} (n=2000, p=5, M=5) over {T} threads, {tt:.1f} s"}
 
 
@@ -197,6 +221,8 @@ def main():
     n, p, M = cfg.n, cfg.p, cfg.M
     r = M + p
 
+    if world > 1:  # every rank generated the same dataset (§8(e))
+        multi.check_same_dataset(coords, y, X, lam, device=dev)
     ctx = lik.create(local, lik.FLAG_TIMING)
     st = torch.cuda.Stream(dev)
     dc, dy, dX, dp, dl = (torch.tensor(a, device=dev) for a in (coords, y, X, P, lam))
@@ -295,6 +321,10 @@ def main():
                          "algorithmic": "n^3/3 + n^2 r + n r^2 FP64 flops per point (SURVEY §8(d)), "
                                         "x points per launch / launch duration (CUDA events on the launching stream)",
                          "share_of_step": chol_ms / (args.steps * ms_local) if ms_local else None},
+            "matern_build": {  # table + build per step: ρ evaluations and workspace bytes written
+                "evals_per_s": K * n * (n - 1) / 2 / (build_ms / args.steps / 1e3) if build_ms > 0 else None,
+                "gb_per_s_written": K * slot_bytes(n, r) / (build_ms / args.steps / 1e3) / 1e9 if build_ms > 0 else None,
+                "hbm_peak_gbs": hbm_peak()},
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
             "launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
             "gpu_launches": int(sum(v[1] for v in stages.values())),

@@ -13,6 +13,27 @@ from __future__ import annotations
 import numpy as np
 
 
+def dataset_checksum(*arrays) -> int:
+    """A 60-bit checksum of the dataset arrays (SHA-256 of their bytes)."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return int(h.hexdigest()[:15], 16)
+
+
+def check_same_dataset(*arrays, device=None) -> None:
+    """Every rank generated / loaded the same dataset: all-reduce the
+    checksum with MAX over (h, −h); raises on any disagreement."""
+    import torch
+    import torch.distributed as dist
+    h = dataset_checksum(*arrays)
+    t = torch.tensor([h, -h], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if int(t[0]) != h or int(t[1]) != -h:
+        raise RuntimeError("ranks disagree on the dataset")
+
+
 def shard_indices(K: int, rank: int, world: int) -> np.ndarray:
     """Global point indices owned by `rank` (strided assignment)."""
     return np.arange(rank, K, world)

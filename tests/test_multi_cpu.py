@@ -71,3 +71,36 @@ def test_shard_partition_properties():
             sizes = [len(x) for x in parts]
             assert max(sizes) - min(sizes) <= 1
             assert multi.local_count(K, 0, world) == max(sizes)
+
+
+def _check_worker(rank, world, port, same, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coords = np.arange(10.0).reshape(5, 2)
+        y = np.ones(5) + (0 if same else rank * 1e-12)
+        try:
+            multi.check_same_dataset(coords, y)
+            q.put((rank, "ok"))
+        except RuntimeError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("same", [True, False])
+def test_dataset_agreement_world2(same):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_check_worker, args=(r, 2, port, same, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    if same:
+        assert res == {0: "ok", 1: "ok"}
+    else:
+        assert all("disagree" in v for v in res.values())
