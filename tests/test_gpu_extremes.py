@@ -1,0 +1,87 @@
+"""GPU parity at parameter extremes (-m gpu): ranges from far below to far above
+the site spacing, κ from 0.05 to just below the Gaussian switch (R7), strong
+anisotropy in both directions (R5), zero / tiny / large nuggets.  V elementwise
+against the oracle (the Matérn table's per-point octave range, its clamping and
+the exact-path fallbacks), then ℓ_p, with the R11 borderline rule for the
+near-singular matrices some of these produce."""
+import os
+
+import numpy as np
+import pytest
+
+import synthgen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2305_04318_b200 as lik  # noqa: E402
+
+NTHREADS = os.cpu_count() or 8
+
+
+def _extreme_params(spacing):
+    rows = []
+    for phiX in (1e-3 * spacing, 0.3 * spacing, 30 * spacing, 1e4 * spacing):
+        for kappa in (0.05, 0.5, 7.5, 999.0):
+            for nug, phiR, phiA in ((0.0, 1.0, 0.0), (1e-6, 25.0, 0.7), (10.0, 0.04, -1.2)):
+                rows.append([phiX, kappa, nug, phiR, phiA])
+    return np.array(rows)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = lik.create(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_matern_build_extremes(ctx, orc, name):
+    coords, y, X = synthgen.make_dataset(name)
+    d = np.sqrt(((coords[:, None, :] - coords[None, :, :]) ** 2).sum(-1))
+    spacing = float(np.median(np.sort(d, axis=1)[:, 1]))
+    P = _extreme_params(spacing)
+    V = ctx.debug_build_V(torch.tensor(coords, device="cuda"), torch.tensor(P, device="cuda")).cpu().numpy()
+    for k in range(P.shape[0]):
+        ref = orc.build_V(coords, P[k])
+        # as in test_matern_build_elementwise: relative 1e-13·max(1, κ/10) + 2e-15·|ln ρ|,
+        # plus an absolute floor of 1e-20 (V_ii ≥ 1): in the deep tail at κ near the
+        # Gaussian switch the prefactor's cancelling terms (|ln Γ(κ)| ~ 6e3 at κ = 999)
+        # make a per-element relative bar meaningless, and an absolute 1e-20 moves log|V|
+        # and the quadratic forms by ≤ n·1e-20·‖V⁻¹‖ (ℓ_p is checked below)
+        tol = (1e-13 * max(1.0, P[k, 1] / 10.0) if P[k, 1] < 1e3 else 1e-14) \
+            + 2e-15 * np.abs(np.log(np.maximum(ref, 1e-300)))
+        err = np.abs(V[k] - ref) - tol * np.abs(ref)
+        assert err.max() <= 1e-20, (k, P[k].tolist(), float(err.max()))
+
+
+def test_loglik_extremes(ctx, orc):
+    coords, y, X = synthgen.make_dataset("C2")
+    d = np.sqrt(((coords[:, None, :] - coords[None, :, :]) ** 2).sum(-1))
+    spacing = float(np.median(np.sort(d, axis=1)[:, 1]))
+    P = _extreme_params(spacing)
+    lam = np.array([0.0, 0.5, 1.0])
+    g = ctx.eval_batch(coords, y, X, P, lam)
+    r = orc.eval_batch(coords, y, X, P, lam, nthreads=NTHREADS)
+    n = coords.shape[0]
+    both = (g["status"] == 0) & (r["status"] == 0)
+    for k in np.nonzero(g["status"] != r["status"])[0]:
+        # only the R11 non-PD decision may differ, and only within rounding of its threshold
+        assert {int(g["status"][k]), int(r["status"][k])} <= {lik.PT_OK, lik.PT_V_NOT_PD, lik.PT_NEG_RESID}, k
+        _, D, _ = orc.ldl(orc.build_V(coords, P[k]))
+        tol = n * np.finfo(float).eps * (1.0 + P[k, 2])
+        nz = D[D != 0]
+        assert (nz.min() if len(nz) else 0.0) < 100 * tol, (k, P[k].tolist())
+    # well-conditioned points: the north_star bar; ill-conditioned ones (ν² ≈ 0 with long
+    # ranges): FP64 backward error scaled by cond(V) — SURVEY §8(d)'s cond-scaled parity
+    for k in np.nonzero(both)[0]:
+        Vr = orc.build_V(coords, P[k])
+        ev = np.linalg.eigvalsh(Vr)
+        cond = ev[-1] / max(ev[0], 1e-300)
+        tol = max(1e-8, 1e-14 * cond)
+        rel = np.abs(g["loglik"][k] - r["loglik"][k]) / np.abs(r["loglik"][k])
+        assert rel.max() <= tol, (k, P[k].tolist(), float(rel.max()), cond)
+    assert both.sum() >= P.shape[0] // 2
