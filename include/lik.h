@@ -161,6 +161,24 @@ int lik_profiles_device(lik_ctx* ctx, int n, int p, int K, int M, const double* 
 int lik_get_stage_times(lik_ctx* ctx, double* ms, long long* launches);
 int lik_reset_stage_times(lik_ctx* ctx);
 
+/* Prepared datasets: validate and upload (coords, y, X, lambdas) once — host
+ * pointers, the same layouts, validation and error codes as lik_eval_batch —
+ * then evaluate any number of parameter batches on it with
+ * lik_dataset_eval_device: device pointers for params and the outputs (layouts as
+ * in lik_eval_batch), enqueued on `cuda_stream` with no host synchronisation and
+ * no host copy of the data (lik_eval_batch_device validates on the host on every
+ * call).  Results are bitwise identical to lik_eval_batch_device on the same
+ * inputs.  A dataset belongs to the device of the context that created it; it must
+ * outlive the evaluations enqueued on it (destroy only after they completed).
+ * (The paper's workflow: one dataset, many representative-point batches.) */
+typedef struct lik_dataset lik_dataset;
+int lik_dataset_create(lik_ctx* ctx, lik_dataset** out, int n, int p, const double* coords,
+                       const double* y, const double* X, int M, const double* lambdas);
+int lik_dataset_eval_device(lik_ctx* ctx, const lik_dataset* ds, int K, const double* params,
+                            double* loglik, double* betahat, double* sigma2hat, double* logdetV,
+                            int* status, void* cuda_stream);
+void lik_dataset_destroy(lik_dataset* ds);
+
 /* Points per wave, i.e. per build/factor launch (0 = automatic: the fewest
  * waves of at most 16 × (2 × #SMs) points within half the free HBM, each a
  * multiple of 2 × #SMs except the last;

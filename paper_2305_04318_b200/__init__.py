@@ -29,7 +29,8 @@ STAGES = ("prep", "setup", "matern_build", "chol_fused")
 ABI_SYMBOLS = ("lik_create", "lik_destroy", "lik_last_error", "lik_eval_batch",
                "lik_eval_batch_device", "lik_get_stage_times", "lik_reset_stage_times",
                "lik_set_wave_points", "lik_debug_build_V", "lik_eval_batch_device_ex",
-               "lik_profiles_device")
+               "lik_profiles_device", "lik_dataset_create", "lik_dataset_eval_device",
+               "lik_dataset_destroy")
 
 _lib = None
 _PD = ctypes.POINTER(ctypes.c_double)
@@ -75,6 +76,12 @@ def lib():
         L.lik_set_wave_points.restype = i
         L.lik_debug_build_V.argtypes = [_VP, i, _VP, i, _VP, _VP]
         L.lik_debug_build_V.restype = i
+        L.lik_dataset_create.argtypes = [_VP, ctypes.POINTER(_VP), i, i, _VP, _VP, _VP, i, _VP]
+        L.lik_dataset_create.restype = i
+        L.lik_dataset_eval_device.argtypes = [_VP, _VP, i, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
+        L.lik_dataset_eval_device.restype = i
+        L.lik_dataset_destroy.argtypes = [_VP]
+        L.lik_dataset_destroy.restype = None
         _lib = L
     return _lib
 
@@ -156,6 +163,10 @@ class Ctx:
                     sigma2hat=torch.empty((K, M), **f), logdetV=torch.empty(K, **f),
                     status=torch.empty(K, dtype=torch.int32, device=device))
 
+    def dataset(self, coords, y, X, lambdas) -> "Dataset":
+        """lik_dataset_create: validate and upload (coords, y, X, lambdas) once."""
+        return Dataset(self, coords, y, X, lambdas)
+
     def eval_batch_device(self, coords, y, X, params, lambdas, out=None, stream=None):
         """lik_eval_batch_device on torch CUDA float64 tensors (enqueued on `stream`)."""
         import torch
@@ -234,6 +245,51 @@ class Ctx:
 
     def reset_stage_times(self):
         self._check(lib().lik_reset_stage_times(self._h))
+
+
+class Dataset:
+    """A prepared, device-resident dataset (lik_dataset): evaluations on it are enqueued
+    with no host synchronisation."""
+
+    def __init__(self, ctx: "Ctx", coords, y, X, lambdas):
+        coords, y, lambdas = _np(coords), _np(y), _np(lambdas)
+        X = _np(X)
+        if X.ndim == 1:
+            X = X[:, None]
+        self.ctx = ctx
+        self.n, self.p = X.shape
+        self.M = lambdas.shape[0]
+        self._h = _VP()
+        rc = lib().lik_dataset_create(ctx._h, ctypes.byref(self._h), self.n, self.p, _ptr(coords),
+                                      _ptr(y), _ptr(X), self.M, _ptr(lambdas))
+        ctx._check(rc)
+
+    def eval_device(self, params, out=None, stream=None):
+        """lik_dataset_eval_device: params a K×5 torch CUDA float64 tensor; outputs as in
+        Ctx.eval_batch_device, enqueued on `stream` (default: the current stream)."""
+        import torch
+        K = params.shape[0]
+        if out is None:
+            out = Ctx.alloc_outputs(K, self.M, self.p, params.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(params.device)
+        rc = lib().lik_dataset_eval_device(
+            self.ctx._h, self._h, K, _tptr(params), _tptr(out["loglik"]), _tptr(out["betahat"]),
+            _tptr(out["sigma2hat"]), _tptr(out["logdetV"]), _tptr(out["status"]),
+            ctypes.c_void_p(stream.cuda_stream))
+        self.ctx._check(rc)
+        return out
+
+    def close(self):
+        if self._h:
+            lib().lik_dataset_destroy(self._h)
+            self._h = _VP()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def create(device: int = 0, flags: int = 0) -> Ctx:

@@ -51,6 +51,16 @@ struct lik_ctx {
   std::vector<cudaEvent_t> ev;
 };
 
+// A validated, device-resident dataset (lik_dataset_create): the per-call prep
+// products, made once, so repeated evaluations need no host work.
+struct lik_dataset {
+  int device = 0, n = 0, p = 0, M = 0;
+  double* coords_p = nullptr;  // sites in Morton order
+  double* bt = nullptr;        // Bᵀ rows (r × npad)
+  double* S = nullptr;         // Σ log y, d²min, d²max
+  double* lambdas = nullptr;   // M
+};
+
 namespace {
 
 int fail(lik_ctx* c, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
@@ -199,10 +209,18 @@ struct Extras {
          *loglik_reml = nullptr, *sigma2hat_reml = nullptr;
 };
 
+// The per-call prep products (sites in Morton order, Bᵀ rows, Σ log y and the
+// distance range), when a prepared dataset (lik_dataset) supplies them.
+struct Prepared {
+  const double* coords_p;
+  const double* bt;
+  const double* S;
+};
+
 int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, const double* X,
                int K, const double* params, int M, const double* lambdas, double* loglik,
                double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st,
-               const double* hcoords, const Extras& ex = Extras()) {
+               const double* hcoords, const Extras& ex = Extras(), const Prepared* pre = nullptr) {
   HostTrace tr;
   const SlotGeom g = lik::make_geom(n, M + p);
   const size_t slot_bytes = g.slot_d * sizeof(double);
@@ -239,38 +257,47 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   size_t pcb = c->pc_cap * sizeof(PointConst);
   if ((rc = ensure(c, &c->pc, &pcb, (size_t)K * sizeof(PointConst)))) return rc;
   c->pc_cap = pcb / sizeof(PointConst);
-  if ((rc = ensure(c, &c->bt, &c->bt_bytes, (size_t)g.r * g.nt * lik::TB * sizeof(double) + 64)))
-    return rc;
-  if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));  // Σ log y, d²min, d²max
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)W * lik::TABLE_D * sizeof(double))))
     return rc;
-
-  if ((rc = ensure(c, &c->coords_p, &c->coords_p_bytes, (size_t)n * 2 * sizeof(double)))) return rc;
-  tr.mark("ensure");
-  const int* dperm = nullptr;
-  if (!(c->flags & LIK_FLAG_NATURAL_ORDER)) {
-    morton_order(n, hcoords, c->hperm);
-    if ((rc = ensure(c, &c->perm, &c->perm_bytes, (size_t)n * sizeof(int)))) return rc;
-    CUDA_TRY(c, cudaMemcpyAsync(c->perm, c->hperm.data(), (size_t)n * sizeof(int),
-                                cudaMemcpyHostToDevice, st));
-    dperm = c->perm;
-  }
-  tr.mark("morton+h2d");
-
   const bool timing = c->flags & LIK_FLAG_TIMING;
   const int nwaves = (K + W - 1) / W;
   size_t ei = 0;
-  if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
-  CUDA_TRY(c, lik::launch_prep(coords, y, X, lambdas, dperm, n, p, M, g.nt * lik::TB, c->coords_p,
-                               c->bt, c->S, st));
-  CUDA_TRY(c, lik::launch_dist_range(c->coords_p, n, c->S + 1, st));
+  const double *coords_p, *bt, *S;
+  if (pre) {  // prepared dataset: no host work, no prep launches
+    coords_p = pre->coords_p;
+    bt = pre->bt;
+    S = pre->S;
+    if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+  } else {
+    if ((rc = ensure(c, &c->bt, &c->bt_bytes, (size_t)g.r * g.nt * lik::TB * sizeof(double) + 64)))
+      return rc;
+    if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));  // Σ log y, d²min, d²max
+    if ((rc = ensure(c, &c->coords_p, &c->coords_p_bytes, (size_t)n * 2 * sizeof(double)))) return rc;
+    tr.mark("ensure");
+    const int* dperm = nullptr;
+    if (!(c->flags & LIK_FLAG_NATURAL_ORDER)) {
+      morton_order(n, hcoords, c->hperm);
+      if ((rc = ensure(c, &c->perm, &c->perm_bytes, (size_t)n * sizeof(int)))) return rc;
+      CUDA_TRY(c, cudaMemcpyAsync(c->perm, c->hperm.data(), (size_t)n * sizeof(int),
+                                  cudaMemcpyHostToDevice, st));
+      dperm = c->perm;
+    }
+    tr.mark("morton+h2d");
+    if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+    CUDA_TRY(c, lik::launch_prep(coords, y, X, lambdas, dperm, n, p, M, g.nt * lik::TB, c->coords_p,
+                                 c->bt, c->S, st));
+    CUDA_TRY(c, lik::launch_dist_range(c->coords_p, n, c->S + 1, st));
+    coords_p = c->coords_p;
+    bt = c->bt;
+    S = c->S;
+  }
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   for (int w = 0; w < nwaves; ++w) {
     const int k0 = w * W, kw = std::min(W, K - k0);
-    CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, c->S + 1, st));
-    CUDA_TRY(c, lik::launch_build(c->coords_p, g, c->pc, k0, kw, c->table, c->bt, c->ws, st));
+    CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, S + 1, st));
+    CUDA_TRY(c, lik::launch_build(coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
     a.ws = c->ws;
@@ -280,7 +307,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     a.pc = c->pc;
     a.k0 = k0;
     a.lambdas = lambdas;
-    a.S = c->S;
+    a.S = S;
     a.loglik = loglik;
     a.betahat = betahat;
     a.sigma2hat = sigma2hat;
@@ -301,7 +328,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     c->stage_ms[LIK_STAGE_PREP] += ms;
-    c->stage_n[LIK_STAGE_PREP] += 3;  // prep, dist_init, dist_range
+    c->stage_n[LIK_STAGE_PREP] += pre ? 0 : 3;  // prep, dist_init, dist_range
     cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
     c->stage_ms[LIK_STAGE_SETUP] += ms;
     c->stage_n[LIK_STAGE_SETUP] += 1;
@@ -506,6 +533,96 @@ int lik_reset_stage_times(lik_ctx* c) {
     c->stage_n[s] = 0;
   }
   return LIK_OK;
+}
+
+int lik_dataset_create(lik_ctx* c, lik_dataset** out, int n, int p, const double* coords,
+                       const double* y, const double* X, int M, const double* lambdas) {
+  if (!c) return LIK_EINVAL;
+  c->err.clear();
+  if (!out) return fail(c, LIK_EINVAL, "NULL pointer argument");
+  *out = nullptr;
+  if (any_null({coords, y, X, lambdas})) return fail(c, LIK_EINVAL, "NULL pointer argument");
+  int rc = validate(c, n, p, coords, y, X, 1, M, lambdas);
+  if (rc) return rc;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const SlotGeom g = lik::make_geom(n, M + p);
+  const int npad = g.nt * lik::TB;
+  lik_dataset* ds = new lik_dataset;
+  ds->device = c->device;
+  ds->n = n;
+  ds->p = p;
+  ds->M = M;
+  double *dc = nullptr, *dy = nullptr, *dX = nullptr;
+  int* dperm = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(dc);
+    cudaFree(dy);
+    cudaFree(dX);
+    cudaFree(dperm);
+  };
+  cudaError_t e = cudaSuccess;
+  if ((e = cudaMalloc(&ds->coords_p, (size_t)n * 2 * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&ds->bt, (size_t)g.r * npad * sizeof(double) + 64)) != cudaSuccess ||
+      (e = cudaMalloc(&ds->S, 4 * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&ds->lambdas, (size_t)M * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&dc, (size_t)n * 2 * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&dy, (size_t)n * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&dX, (size_t)n * p * sizeof(double))) != cudaSuccess) {
+    cleanup();
+    lik_dataset_destroy(ds);
+    return fail(c, LIK_ENOMEM, "dataset allocation: %s", cudaGetErrorString(e));
+  }
+  const cudaStream_t st = c->own_stream;
+  const int* pperm = nullptr;
+  std::vector<int> hperm;
+  if (!(c->flags & LIK_FLAG_NATURAL_ORDER)) {
+    morton_order(n, coords, hperm);
+    if ((e = cudaMalloc(&dperm, (size_t)n * sizeof(int))) == cudaSuccess)
+      e = cudaMemcpyAsync(dperm, hperm.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice, st);
+    pperm = dperm;
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dc, coords, (size_t)n * 2 * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dy, y, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dX, X, (size_t)n * p * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ds->lambdas, lambdas, (size_t)M * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = lik::launch_prep(dc, dy, dX, ds->lambdas, pperm, n, p, M, npad, ds->coords_p, ds->bt, ds->S, st);
+  if (e == cudaSuccess) e = lik::launch_dist_range(ds->coords_p, n, ds->S + 1, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cleanup();
+  if (e != cudaSuccess) {
+    lik_dataset_destroy(ds);
+    return fail(c, LIK_ECUDA, "dataset preparation: %s", cudaGetErrorString(e));
+  }
+  *out = ds;
+  return LIK_OK;
+}
+
+int lik_dataset_eval_device(lik_ctx* c, const lik_dataset* ds, int K, const double* params,
+                            double* loglik, double* betahat, double* sigma2hat, double* logdetV,
+                            int* status, void* cuda_stream) {
+  if (!c) return LIK_EINVAL;
+  c->err.clear();
+  if (!ds || any_null({params, loglik, betahat, sigma2hat, logdetV, status}))
+    return fail(c, LIK_EINVAL, "NULL pointer argument");
+  if (K < 1) return fail(c, LIK_EINVAL, "K = %d < 1", K);
+  if (ds->device != c->device)
+    return fail(c, LIK_EINVAL, "dataset lives on device %d, context on %d", ds->device, c->device);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const Prepared pre{ds->coords_p, ds->bt, ds->S};
+  return run_device(c, ds->n, ds->p, nullptr, nullptr, nullptr, K, params, ds->M, ds->lambdas,
+                    loglik, betahat, sigma2hat, logdetV, status, (cudaStream_t)cuda_stream, nullptr,
+                    Extras(), &pre);
+}
+
+void lik_dataset_destroy(lik_dataset* ds) {
+  if (!ds) return;
+  cudaFree(ds->coords_p);
+  cudaFree(ds->bt);
+  cudaFree(ds->S);
+  cudaFree(ds->lambdas);
+  delete ds;
 }
 
 int lik_set_wave_points(lik_ctx* c, int pts) {

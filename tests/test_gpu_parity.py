@@ -238,6 +238,42 @@ def test_bitwise_repeatability_over_cta_rounds(ctx, name, K, reps):
             assert same, (key, np.nonzero(np.any((first[key] != nxt[key]).reshape(K, -1), axis=1))[0][:10])
 
 
+@pytest.mark.parametrize("name, K", [("C2", 300), ("C4", 900)])
+def test_dataset_api_bitwise(ctx, name, K):
+    """lik_dataset_eval_device: bitwise equal to lik_eval_batch_device; two evaluations
+    enqueued back to back without synchronisation each equal their separate result."""
+    coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
+    t = [torch.tensor(v, device="cuda") for v in (coords, y, X, P, lam)]
+    ref = {k: v.cpu().numpy() for k, v in ctx.eval_batch_device(*t).items()}
+    ds = ctx.dataset(coords, y, X, lam)
+    try:
+        P2 = P[::-1].copy()
+        o1 = ds.eval_device(t[3])
+        o2 = ds.eval_device(torch.tensor(P2, device="cuda"))  # no sync in between
+        torch.cuda.synchronize()
+        for key in ref:
+            assert np.array_equal(o1[key].cpu().numpy(), ref[key], equal_nan=True), key
+            assert np.array_equal(o2[key].cpu().numpy(), ref[key][::-1], equal_nan=True), key
+    finally:
+        ds.close()
+
+
+def test_dataset_api_errors(ctx):
+    coords, y, X, P, lam = synthgen.make_inputs("C1")
+    bad = y.copy()
+    bad[3] = -1.0
+    with pytest.raises(lik.LikError) as e:
+        ctx.dataset(coords, bad, X, lam)
+    assert e.value.code == lik.LIK_EDOMAIN and "y[3]" in ctx.last_error()
+    ds = ctx.dataset(coords, y, X, lam)
+    try:
+        with pytest.raises(lik.LikError) as e:
+            ds.eval_device(torch.zeros((0, 5), dtype=torch.float64, device="cuda"))
+        assert e.value.code == lik.LIK_EINVAL
+    finally:
+        ds.close()
+
+
 def test_stage_timing_api():
     c = lik.create(0, lik.FLAG_TIMING)
     coords, y, X, P, lam = synthgen.make_inputs("C2", K=200)
