@@ -148,7 +148,7 @@ int lik_eval_batch_device_ex(lik_ctx* ctx, int n, int p, const double* coords, c
  *   sigma_grid Sg     values of σ;  prof_sigma Sg: max over (k, m) of ℓ(σ, β̂)
  *              (Eq. profileSigma)
  *   prof_lambda M     max over k of ℓ_p(ω_k, λ_m)
- * Limits: 1 ≤ p ≤ 32, G ≥ 0, Sg ≥ 0.  Returns LIK_OK, LIK_EINVAL, LIK_ENOMEM, LIK_ECUDA. */
+ * Limits: 1 ≤ p ≤ 32, G ≥ 0, Sg ≥ 0, K·M ≤ 2³⁰, K·(p+1) ≤ 2³⁰.  Returns LIK_OK, LIK_EINVAL, LIK_ENOMEM, LIK_ECUDA. */
 int lik_profiles_device(lik_ctx* ctx, int n, int p, int K, int M, const double* y,
                         const double* ssqYX, const double* logdetV, const int* status,
                         const double* lambdas, int G, const double* beta_grid, double* prof_beta,

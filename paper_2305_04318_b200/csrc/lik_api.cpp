@@ -501,19 +501,18 @@ int lik_profiles_device(lik_ctx* c, int n, int p, int K, int M, const double* y,
   if (any_null({y, ssqYX, logdetV, status, lambdas, prof_lambda}) ||
       (G > 0 && (!beta_grid || !prof_beta)) || (Sg > 0 && (!sigma_grid || !prof_sigma)))
     return fail(c, LIK_EINVAL, "NULL pointer argument");
+  if ((long long)K * M > (1LL << 30) || (long long)K * (p + 1) > (1LL << 30))
+    return fail(c, LIK_EINVAL, "K*M=%lld exceeds 2^30", (long long)K * M);
   if (p < 1 || p > 32 || n < p + 2 || K < 1 || M < 1 || G < 0 || Sg < 0)
     return fail(c, LIK_EINVAL, "bad sizes n=%d p=%d K=%d M=%d G=%d Sg=%d (1 <= p <= 32)", n, p, K, M,
                 G, Sg);
   CUDA_TRY(c, cudaSetDevice(c->device));
-  const size_t need = ((size_t)K * p * M * 3 + (size_t)K * M + 2) * sizeof(double);
+  const size_t need = lik::profile_scratch(p, K, M, G, Sg) * sizeof(double);
   int rc;
   if ((rc = ensure(c, &c->prof_scratch, &c->prof_scratch_bytes, need))) return rc;
-  double* coefs = c->prof_scratch;
-  double* qfull = coefs + (size_t)K * p * M * 3;
-  double* S = qfull + (size_t)K * M;
   CUDA_TRY(c, lik::launch_profiles(n, p, K, M, y, ssqYX, logdetV, status, lambdas, G, beta_grid,
-                                   prof_beta, Sg, sigma_grid, prof_sigma, prof_lambda, coefs, qfull,
-                                   S, (cudaStream_t)cuda_stream));
+                                   prof_beta, Sg, sigma_grid, prof_sigma, prof_lambda,
+                                   c->prof_scratch, (cudaStream_t)cuda_stream));
   return LIK_OK;
 }
 

@@ -149,11 +149,14 @@ struct CholArgs {
 };
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
 size_t chol_smem_bytes();
+int profile_slices(long long K, int M);                       // slices of the (k, m) range
+size_t profile_partials(int p, int G, int Sg, int M, int nsl);  // doubles of partial maxima
+size_t profile_scratch(int p, int K, int M, int G, int Sg);     // doubles of scratch
 cudaError_t launch_profiles(int n, int p, int K, int M, const double* y, const double* ssqYX,
                             const double* logdetV, const int* status, const double* lambdas,
                             int G, const double* beta_grid, double* prof_beta, int Sg,
                             const double* sigma_grid, double* prof_sigma, double* prof_lambda,
-                            double* coefs, double* qfull, double* S, cudaStream_t st);
+                            double* scratch, cudaStream_t st);
 int chol_ctas_per_sm();
 
 }  // namespace lik
