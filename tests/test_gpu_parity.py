@@ -221,6 +221,26 @@ def test_determinism_waves_and_apis(ctx):
         assert np.array_equal(a[key], out[key].cpu().numpy(), equal_nan=True), key
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_assembly_bitwise_vs_one_gpu(ctx, world):
+    """§8(e): the sharded table equals the 1-GPU table bitwise.  Each rank's strided
+    shard is evaluated in turn on this one GPU (independent calls, no collective),
+    packed as all_gather_results packs it and un-strided by unpack_global."""
+    from paper_2305_04318_b200 import multi
+    coords, y, X, P, lam = synthgen.make_inputs("C2", K=301)
+    K, M, p = P.shape[0], len(lam), X.shape[1]
+    dc, dy, dX, dl = (torch.tensor(v, device="cuda") for v in (coords, y, X, lam))
+    full = ctx.eval_batch_device(dc, dy, dX, torch.tensor(P, device="cuda"), dl)
+    Kmax = multi.local_count(K, 0, world)
+    bufs = []
+    for g in range(world):
+        out = ctx.eval_batch_device(dc, dy, dX, torch.tensor(P[multi.shard_indices(K, g, world)], device="cuda"), dl)
+        bufs.append(multi.pack(out, M, p, Kmax))
+    table = multi.unpack_global(torch.stack(bufs).cpu().numpy(), K, M, p, world)
+    for key in table:
+        assert np.array_equal(table[key], full[key].cpu().numpy(), equal_nan=True), (world, key)
+
+
 @pytest.mark.parametrize("name, K, reps", [("C3", 1776, 3), ("C4", 1184, 2)])
 def test_bitwise_repeatability_over_cta_rounds(ctx, name, K, reps):
     """Repeated calls give bitwise identical outputs with several rounds of resident
