@@ -7,18 +7,12 @@ values, λ), 1 GPU.  The paper reports no timings for these runs."
 import json, math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-import synthgen, paper_2305_04318_b200 as lik
+import paper_2305_04318_b200 as lik
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from paper_2305_04318_b200 import representative as rp
 
 
-def workload(name, n, p, K, M, seed):
-    cfg = synthgen.Config(name, n, min(p, 5), K, M, False, "uniform", name)
-    coords, y, X5 = synthgen.make_dataset(cfg, seed=seed)
-    rng = np.random.default_rng(seed)
-    X = np.column_stack([X5] + [rng.normal(size=n) for _ in range(p - X5.shape[1])])
-    P = synthgen.make_params(cfg, K, seed=seed + 1)
-    lam = np.linspace(0.2, 0.8, M)
-    return coords, y, X, P, lam
+from bench_paper_workloads_lib import workload  # noqa: E402
 
 
 ctx = lik.create(0, lik.FLAG_TIMING)
