@@ -85,3 +85,34 @@ def test_loglik_extremes(ctx, orc):
         rel = np.abs(g["loglik"][k] - r["loglik"][k]) / np.abs(r["loglik"][k])
         assert rel.max() <= tol, (k, P[k].tolist(), float(rel.max()), cond)
     assert both.sum() >= P.shape[0] // 2
+
+
+@pytest.mark.parametrize("n", [4097, 12000, 16385])
+def test_ou_closed_form_large_n(ctx, orc, n):
+    """Largest sizes, pinned without the O(n³) oracle: κ = ½, ν² = 0 on collinear
+    sites is the Ornstein-Uhlenbeck covariance with a tridiagonal inverse, so ℓ_p,
+    β̂, σ̂² and log|V| have an O(n) closed form (tests/closed_forms.py; the same pin
+    as the oracle's at n = 50, 600).  n = 12,000 is 188 tiles with a 32-row tail,
+    n = 16,385 256 full tiles and a 1-row tail;
+    three points with different ranges / anisotropy run in one launch."""
+    from closed_forms import ou_loglik
+    rng = np.random.default_rng(n)
+    u = np.array([np.cos(1.1), np.sin(1.1)])
+    pts = [[300.0, 0.5, 0.0, 2.5, 0.6], [80.0, 0.5, 0.0, 1.0, 0.0], [1500.0, 0.5, 0.0, 0.3, -1.0]]
+    # spacing so that r_i = exp(−2 g Δt) ≤ 0.9 for every point (g ≤ g_max)
+    gs = [orc.aniso_distance(u[0], u[1], *np.array(w)[[0, 3, 4]]) for w in pts]
+    gaps = rng.uniform(-np.log(0.9) / (2 * min(gs)), 3.0 / min(gs), size=n - 1)
+    t = rng.permutation(np.concatenate([[0.0], np.cumsum(gaps)]))
+    coords = np.outer(t, u) + np.array([1234.5, -987.0])
+    X = np.column_stack([np.ones(n), rng.normal(size=n), rng.normal(size=n)])
+    y = np.exp(rng.normal(2.0, 0.3, size=n))
+    lam = np.array([0.0, 0.5])
+    out = ctx.eval_batch(coords, y, X, np.array(pts), lam)
+    assert (out["status"] == 0).all()
+    for k, g in enumerate(gs):
+        for m, l in enumerate(lam):
+            ll, beta, s2, ld = ou_loglik(t, g, y, X, l)
+            assert out["logdetV"][k] == pytest.approx(ld, rel=1e-9), (k, m)
+            assert out["loglik"][k, m] == pytest.approx(ll, rel=1e-10), (k, m)
+            np.testing.assert_allclose(out["betahat"][k, m], beta, rtol=1e-8, atol=1e-9)
+            assert out["sigma2hat"][k, m] == pytest.approx(s2, rel=1e-9)

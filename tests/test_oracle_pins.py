@@ -18,6 +18,7 @@ import os
 import mpmath
 import numpy as np
 import pytest
+from closed_forms import ou_loglik  # noqa: E402
 import scipy.linalg as sla
 import scipy.stats as sst
 
@@ -289,27 +290,6 @@ def test_brute_force_mpmath_small(orc):
             assert out["logdetV"][0] == pytest.approx(ld, rel=1e-11, abs=1e-12)
 
 
-def _ou_loglik(t, g, y, X, lam):
-    """κ = 1/2, ν² = 0, collinear sites: V_ij = exp(−2 g |t_i − t_j|) is the
-    covariance of a stationary Ornstein-Uhlenbeck process, whose inverse is
-    tridiagonal: log|V| = Σ log(1 − r_i²),
-    aᵀV⁻¹b = a_1 b_1 + Σ (a_{i+1} − r_i a_i)(b_{i+1} − r_i b_i)/(1 − r_i²)."""
-    o = np.argsort(t)
-    t, y, X = t[o], y[o], X[o]
-    r = np.exp(-2 * g * np.diff(t))
-    yp = np.log(y) if lam == 0 else (y ** lam - 1) / lam
-    B = np.column_stack([yp, X])
-    W = np.vstack([B[:1], (B[1:] - r[:, None] * B[:-1]) / np.sqrt(1 - r * r)[:, None]])
-    C = W.T @ W
-    XX, Xy, yy = C[1:, 1:], C[1:, 0], C[0, 0]
-    beta = np.linalg.solve(XX, Xy)
-    q = yy - Xy @ beta
-    n = len(y)
-    logdet = np.log1p(-r * r).sum()
-    m2l = n * np.log(q / n) + logdet - 2 * (lam - 1) * np.log(y).sum() + n * np.log(2 * np.pi) + n
-    return -m2l / 2, beta, q / n, logdet
-
-
 @pytest.mark.parametrize("n", [50, 600])
 def test_ou_closed_form(orc, n):
     rng = np.random.default_rng(n)
@@ -327,7 +307,7 @@ def test_ou_closed_form(orc, n):
     out = orc.eval_batch(coords, y, X, [[phiX, 0.5, 0.0, phiR, phiA]], lam)
     assert out["status"][0] == 0
     for m, l in enumerate(lam):
-        ll, beta, s2, ld = _ou_loglik(t, g, y, X, l)
+        ll, beta, s2, ld = ou_loglik(t, g, y, X, l)
         assert out["logdetV"][0] == pytest.approx(ld, rel=1e-10)
         assert out["loglik"][0, m] == pytest.approx(ll, rel=1e-10)
         np.testing.assert_allclose(out["betahat"][0, m], beta, rtol=1e-8, atol=1e-9)
