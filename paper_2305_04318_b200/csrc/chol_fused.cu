@@ -145,34 +145,47 @@ typedef double Acc[MI][NI][2];
 
 // One chunk (KC/4 k-steps of 4) of  acc += A_rows · B_rowsᵀ  for this warp.
 // MFULL: both 8-row groups of the warp are live (the common case), so the DMMA
-// sequence is branch- and predicate-free.
-template <bool MFULL>
+// sequence is branch- and predicate-free.  NL: column groups computed (NI, or fewer
+// for a diagonal tile, whose columns beyond the warp's rows are never read).
+template <bool MFULL, int NL = NI>
 __device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ Ab, int rbase,
                                           int mlim, const double* __restrict__ Bb, int lane) {
   const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
 #pragma unroll
   for (int kk = 0; kk < KC / 4; ++kk) {
     const int kcol = ((kk * 4) ^ sw) + lc;
-    double a[MI], b[NI];
+    double a[MI], b[NL];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) a[mi] = Ab[(rbase + mi * 8 + lr) * KC + kcol];
 #pragma unroll
-    for (int ni = 0; ni < NI; ++ni) b[ni] = Bb[(ni * 8 + lr) * KC + kcol];
+    for (int ni = 0; ni < NL; ++ni) b[ni] = Bb[(ni * 8 + lr) * KC + kcol];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
       if (MFULL || mi < mlim) {
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < NL; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
       }
   }
 }
 
+// nlim < NI only for the warps of a diagonal tile with all rows live: warp rows
+// [rbase, rbase + 16) need the column groups < rbase/8 + 2 (the strict upper
+// triangle beyond them is never read: the factorisation and the Schur block read
+// the lower triangle only).
 __device__ __forceinline__ void mma_chunk_any(Acc& acc, const double* Ab, int rbase, int mlim,
-                                              const double* Bb, int lane) {
-  if (mlim == MI)
-    mma_chunk<true>(acc, Ab, rbase, MI, Bb, lane);
-  else if (mlim > 0)
+                                              int nlim, const double* Bb, int lane) {
+  if (mlim == MI) {
+    if (nlim == NI)
+      mma_chunk<true>(acc, Ab, rbase, MI, Bb, lane);
+    else if (nlim == 2)
+      mma_chunk<true, 2>(acc, Ab, rbase, MI, Bb, lane);
+    else if (nlim == 4)
+      mma_chunk<true, 4>(acc, Ab, rbase, MI, Bb, lane);
+    else
+      mma_chunk<true, 6>(acc, Ab, rbase, MI, Bb, lane);
+  } else if (mlim > 0) {
     mma_chunk<false>(acc, Ab, rbase, mlim, Bb, lane);
+  }
 }
 
 // acc ← acc · Xᵀ in place, X = L⁻¹ (64×64 lower triangular, swizzled shared memory):
@@ -332,7 +345,7 @@ struct Src {
 // At the start of chunk q one warp (rotating) refills the stage of chunk q−1 with
 // chunk q−1+NSTAGE; the first NSTAGE chunks are issued by the lead thread.
 __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
-                                      bool mine_b, int rbase, int mlim, int lane,
+                                      bool mine_b, int rbase, int mlim, int nlim, int lane,
                                       const double* slot_lo, const double* slot_hi) {
   const int tid = threadIdx.x;
   const uint32_t seq = pp.seq;
@@ -387,7 +400,7 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
     if (tid == 224) atomicAdd(&g_lik_phase[q == 0 ? 9 : 15], (unsigned long long)(clock64() - tw0));
 #endif
     const double* st = pp.stages + s * STAGE_D;
-    mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, st + 2 * CHUNK_D, lane);
+    mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, nlim, st + 2 * CHUNK_D, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(saddr(&pp.empty[s]));
   }
@@ -777,11 +790,16 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
       const int ti = sel ? ib : ia;  // −1: this warp has no tile in a single-row block
       const int vmine = ti >= 0 ? valid_rows(ti) : 0;
       const int mlim = max(0, min(MI, (vmine - rbase + 7) >> 3));
+#ifndef LIK_NO_DIAG_SKIP
+      const int nlim = (rb == 0 && sel == 0) ? min(NI, (rbase >> 3) + 2) : NI;  // diagonal tile
+#else
+      const int nlim = NI;
+#endif
       // acc = Σ_k L_ik L_jkᵀ − A_ij = −C
       frag_zero(acc);
       PH(0);
       if (j > 0)
-        kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, lane, ws,
+        kloop(acc, pp, src(ia), src(ib), src(j), CHUNKS * j, mine_b, rbase, mlim, nlim, lane, ws,
               ws + g.slot_d);
       PH(1);
       if (ti >= 0) {
@@ -853,7 +871,7 @@ __global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs
     const int mlim = mine_b ? 0 : max(0, min(MI, (g.Ra - rbase + 7) >> 3));
     frag_zero(acc);
     kloop(acc, pp, src(nt), Src{nullptr, 0, nullptr, 0}, src(nt), CHUNKS * nt, false, rbase, mlim,
-          lane, ws, ws + g.slot_d);
+          NI, lane, ws, ws + g.slot_d);
     __syncthreads();
     frag_store<false>(acc, staging, rbase, mlim, lane);
     __syncthreads();
