@@ -184,6 +184,16 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _reserve_stdout():
+    """Return a stream on the original stdout and send fd 1 to stderr from here on:
+    native libraries (NCCL's version / NCCL_DEBUG lines) write to fd 1 directly, and
+    stdout must carry only the one JSON line."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -192,6 +202,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--points", type=int, default=None, help="points per rank (default 20000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use torch.distributed (NCCL) even with one process: runs the multi-GPU "
+                         "code path (checksum, all-gather, max over ranks) on a single GPU")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -201,6 +214,7 @@ def main():
         run_reference(args, rank, world)
         return
 
+    json_out = _reserve_stdout()
     import torch
     import torch.distributed as dist
 
@@ -209,7 +223,13 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29571")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = synthgen.CONFIGS[WORKLOAD]
@@ -221,7 +241,7 @@ def main():
     n, p, M = cfg.n, cfg.p, cfg.M
     r = M + p
 
-    if world > 1:  # every rank generated the same dataset (§8(e))
+    if use_dist:  # every rank generated the same dataset (§8(e))
         multi.check_same_dataset(coords, y, X, lam, device=dev)
     ctx = lik.create(local, lik.FLAG_TIMING)
     st = torch.cuda.Stream(dev)
@@ -229,11 +249,11 @@ def main():
     out = lik.Ctx.alloc_outputs(K, M, p, dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     pack_w = multi.pack_width(M, p)
-    gathered = torch.empty((world * K, pack_w), dtype=torch.float64, device=dev) if world > 1 else None
+    gathered = torch.empty((world * K, pack_w), dtype=torch.float64, device=dev) if use_dist else None
 
     def step():
         ctx.eval_batch_device(dc, dy, dX, dp, dl, out=out, stream=st)
-        if world > 1:  # the one exchange step: all-gather of the result tables (NCCL / NVLink)
+        if use_dist:  # the one exchange step: all-gather of the result tables (NCCL / NVLink)
             with torch.cuda.stream(st):
                 dist.all_gather_into_tensor(gathered, multi.pack(out, M, p, K))
 
@@ -243,7 +263,7 @@ def main():
         step()
     torch.cuda.synchronize()
     ctx.reset_stage_times()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -258,14 +278,14 @@ def main():
             evs[s][1].record(st)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
-    if world > 1:
+    if use_dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms_local = float(np.mean(step_ms))
     stages = ctx.stage_times()
     # max over ranks
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     total_pts = K * world
@@ -279,19 +299,33 @@ def main():
     e2e_ctx = lik.create(local)
     e2e_ctx.eval_batch(*hn)  # warm (allocations)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     e2e_steps = max(1, min(args.steps, 2))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        res = e2e_ctx.eval_batch(*hn)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if not use_dist:
+        # lik_eval_batch: host inputs in, host outputs back (one C-ABI call)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = e2e_ctx.eval_batch(*hn)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        h2d = sum(a.nbytes for a in hn)
+        d2h = sum(v.nbytes for v in res.values())
+    else:
+        # multi.eval_sharded: this rank's shard up, the all-gathered table of every
+        # rank's results back to the host (the multi-GPU public entry point)
+        multi.eval_sharded(e2e_ctx, coords, y, X, Pall, lam, dev)  # warm
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = multi.eval_sharded(e2e_ctx, coords, y, X, Pall, lam, dev)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        h2d = sum(a.nbytes for a in hn)  # coords, y, X, this rank's params, λ
+        d2h = world * multi.local_count(K * world, 0, world) * pack_w * 8
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = total_pts / float(te.item())
-    h2d = sum(a.nbytes for a in hn)
-    d2h = sum(v.nbytes for v in res.values())
     e2e_ctx.close()
 
     if rank == 0:
@@ -336,9 +370,9 @@ def main():
         }
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(coords, y, X, P, lam)
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     ctx.close()
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

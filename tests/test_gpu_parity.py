@@ -388,3 +388,20 @@ def test_bounds_checked_build():
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "lik bounds" not in r.stdout + r.stderr
+
+
+def test_eval_sharded_nccl_world1(ctx):
+    """multi.eval_sharded (the multi-GPU entry point: shard, evaluate, NCCL all-gather,
+    un-stride) under a one-rank NCCL group equals eval_batch bitwise."""
+    import torch.distributed as dist
+    from paper_2305_04318_b200 import multi
+    coords, y, X, P, lam = synthgen.make_inputs("C2", K=77)
+    ref = ctx.eval_batch(coords, y, X, P, lam)
+    store = dist.HashStore()
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        got = multi.eval_sharded(ctx, coords, y, X, P, lam, torch.device("cuda", 0))
+    finally:
+        dist.destroy_process_group()
+    for key in ref:
+        assert np.array_equal(ref[key], got[key], equal_nan=True), key
