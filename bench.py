@@ -333,9 +333,14 @@ def main():
         build_ms, build_n = stages["matern_build"]
         peak, peak_src = fp64_peak()
         achieved = (args.steps * K * F) / (chol_ms / 1e3) / 1e12 if chol_ms > 0 else None
-        traffic = None
+        traffic, traffic_note = None, None
         try:
-            traffic = json.load(open(TRAFFIC)).get("dram_bytes_per_launch")
+            tj = json.load(open(TRAFFIC))
+            pts_per_launch = args.steps * K / chol_n if chol_n else K
+            traffic = tj["dram_bytes_per_point"] * pts_per_launch
+            traffic_note = (f"dram_bytes_read+write per point from one ncu --set full capture "
+                            f"({tj['points_per_launch']}-point launch, {tj['source']}) x "
+                            f"{pts_per_launch:.0f} points per launch here")
         except Exception:
             pass
         line = {
@@ -351,6 +356,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "chol_fused (DMMA.8x8x4)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "traffic_note": traffic_note,
                          "peak_source": peak_src,
                          "algorithmic": "n^3/3 + n^2 r + n r^2 FP64 flops per point (SURVEY §8(d)), "
                                         "x points per launch / launch duration (CUDA events on the launching stream)",
