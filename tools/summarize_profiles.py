@@ -24,7 +24,7 @@ for r in rows[hdr_i + 1:]:
 tot = sum(v[0] for v in agg.values())
 with open(os.path.join(dst, "launch_shares.txt"), "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
-    f.write("command: python bench.py --points 592 --steps 1 --warmup 3 --no-cpu-baseline\n")
+    f.write("command: python bench.py (the default bench run: 3 warm-up + 3 timed steps of C4)\n")
     for k, (t, n) in sorted(agg.items(), key=lambda x: -x[1][0]):
         f.write(f"{k[:60]:60s} launches={n:5d} total_ms={t/1e6:10.3f} share={t/tot:6.3f}\n")
 subprocess.run(["cp", os.path.join(src, "launches.csv"), os.path.join(dst, "launches.csv")])
