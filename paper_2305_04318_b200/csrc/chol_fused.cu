@@ -147,10 +147,51 @@ typedef double Acc[MI][NI][2];
 // MFULL: both 8-row groups of the warp are live (the common case), so the DMMA
 // sequence is branch- and predicate-free.  NL: column groups computed (NI, or fewer
 // for a diagonal tile, whose columns beyond the warp's rows are never read).
+#ifndef LIK_KPAIR
+#define LIK_KPAIR 1
+#endif
 template <bool MFULL, int NL = NI>
 __device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ Ab, int rbase,
                                           int mlim, const double* __restrict__ Bb, int lane) {
   const int lr = lane >> 2, lc = lane & 3, sw = swz(lr);
+#if LIK_KPAIR
+  // Two k-steps per 16-byte load: within each group of 8 columns, the first step
+  // takes the even columns and the second the odd ones (each column once, the same
+  // assignment for A and B), so lane lc needs the adjacent pair (2lc, 2lc+1) — one
+  // LDS.128.  The swizzle XORs multiples of 4, so the pair stays adjacent and
+  // aligned; rows with (r & 3) < 2 and ≥ 2 fall in opposite bank halves (4
+  // wavefronts per 512 bytes: conflict-free).  B fragments in two halves of NL/2
+  // keep the live registers close to the one-step form.
+  static_assert(KC % 8 == 0, "k pairs");
+#pragma unroll
+  for (int kp = 0; kp < KC / 8; ++kp) {
+    const int kcol = ((kp * 8 + 2 * lc) ^ sw);
+    double2 a[MI];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+      a[mi] = *reinterpret_cast<const double2*>(Ab + (rbase + mi * 8 + lr) * KC + kcol);
+    constexpr int NH = NL >= 4 ? NL / 2 : NL;
+#pragma unroll
+    for (int h = 0; h < NL / NH; ++h) {
+      double2 b[NH];
+#pragma unroll
+      for (int q = 0; q < NH; ++q)
+        b[q] = *reinterpret_cast<const double2*>(Bb + ((h * NH + q) * 8 + lr) * KC + kcol);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+        if (MFULL || mi < mlim) {
+#pragma unroll
+          for (int q = 0; q < NH; ++q) dmma(acc[mi][h * NH + q], a[mi].x, b[q].x);
+        }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+        if (MFULL || mi < mlim) {
+#pragma unroll
+          for (int q = 0; q < NH; ++q) dmma(acc[mi][h * NH + q], a[mi].y, b[q].y);
+        }
+    }
+  }
+#else
 #pragma unroll
   for (int kk = 0; kk < KC / 4; ++kk) {
     const int kcol = ((kk * 4) ^ sw) + lc;
@@ -166,6 +207,7 @@ __device__ __forceinline__ void mma_chunk(Acc& acc, const double* __restrict__ A
         for (int ni = 0; ni < NL; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
       }
   }
+#endif
 }
 
 // nlim < NI only for the warps of a diagonal tile with all rows live: warp rows
