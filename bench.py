@@ -55,7 +55,9 @@ def fp64_peak():
     try:
         vals = [json.loads(l) for l in open(PHASE0)]
         best = max(v["tflops"] for v in vals if v.get("kind") == "dmma_sustained")
-        return best, "measured: DMMA.8x8x4 loop, tools/phase0 (profiles/r01/phase0_fp64_peaks.jsonl)"
+        return best, ("measured: DMMA.8x8x4 loop, tools/phase0 (profiles/r01/phase0_fp64_peaks.jsonl); "
+                      "MEASURED_PEAKS.json has no FP64 entry and its bf16 x nominal-ratio route "
+                      "(~27 TF/s) is below what this kernel sustains (DESIGN.md sec. 5)")
     except Exception:
         return 37.2, "nominal: 148 SM x 64 FMA/clk x 2 x 1.965 GHz"
 
