@@ -148,8 +148,10 @@ def cpu_baseline(coords, y, X, P, lam, budget_s=20.0):
         oracle.eval_batch(coords, y, X, P[T:T * rounds], lam, nthreads=T)
         tt += time.perf_counter() - t0
         npts += T * (rounds - 1)
+    K_full = synthgen.CONFIGS[WORKLOAD].K
     return {"value": npts / tt, "unit": UNIT, "cores": T, "kind": "oracle", "cpu_model": cpu_model(),
-            "sample": f"{npts} points of {WORKLOAD} (n=2000, p=5, M=5) over {T} threads, {tt:.1f} s"}
+            "sample": f"{npts} points of {WORKLOAD} (n=2000, p=5, M=5) over {T} threads, {tt:.1f} s",
+            "extrapolated_full_config_hours": K_full / (npts / tt) / 3600.0}
 
 
 def run_reference(args, rank, world):
