@@ -754,7 +754,12 @@ __device__ void write_point_failure(const CholArgs& A, int k, int code) {
 #ifndef LIK_MIN_BLOCKS
 #define LIK_MIN_BLOCKS 2
 #endif
-__global__ void __launch_bounds__(NT, LIK_MIN_BLOCKS) chol_fused_kernel(CholArgs A) {
+#ifdef LIK_CHOL_MAXREG  // experiment: a register cap below the 2-CTA/SM one
+#define LIK_CHOL_BOUNDS __maxnreg__(LIK_CHOL_MAXREG)
+#else
+#define LIK_CHOL_BOUNDS __launch_bounds__(NT, LIK_MIN_BLOCKS)
+#endif
+__global__ void LIK_CHOL_BOUNDS chol_fused_kernel(CholArgs A) {
   extern __shared__ __align__(1024) double sm[];
 #ifdef LIK_CTA_TRACE
   const unsigned long long t_start = gtimer();
