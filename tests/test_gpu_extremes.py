@@ -116,3 +116,43 @@ def test_ou_closed_form_large_n(ctx, orc, n):
             assert out["loglik"][k, m] == pytest.approx(ll, rel=1e-10), (k, m)
             np.testing.assert_allclose(out["betahat"][k, m], beta, rtol=1e-8, atol=1e-9)
             assert out["sigma2hat"][k, m] == pytest.approx(s2, rel=1e-9)
+
+
+@pytest.mark.parametrize("n, aniso", [(1500, False), (700, True)])
+def test_kappa_3_2_closed_form_lapack(ctx, orc, n, aniso):
+    """κ = 3/2: the paper's Matérn (P:100-103 with R1) is exactly ρ = (1 + z) e^{−z},
+    z = √12 d, so V is known in closed form; ℓ_p, β̂, σ̂², log|V| of the CUDA path
+    against that V factored by LAPACK (numpy) — independent of the oracle's
+    arithmetic and of the kernels.  d from the oracle's pinned anisotropic distance
+    (SPEC examples) in the anisotropic case."""
+    rng = np.random.default_rng(n)
+    side = 9000.0 * np.sqrt(n / 224)
+    coords = rng.uniform(0, side, size=(n, 2))
+    phiX, nug = 900.0, 0.3
+    phiR, phiA = (2.0, 0.7) if aniso else (1.0, 0.0)
+    h = coords[:, None, :] - coords[None, :, :]
+    if aniso:
+        dist = np.vectorize(lambda a, b: orc.aniso_distance(a, b, phiX, phiR, phiA))
+        d = dist(h[..., 0], h[..., 1])
+    else:
+        d = np.hypot(h[..., 0], h[..., 1]) / phiX
+    z = np.sqrt(12.0) * d
+    V = (1.0 + z) * np.exp(-z) + nug * np.eye(n)
+    X = np.column_stack([np.ones(n), coords[:, 0] / side, rng.normal(size=n)])
+    y = np.exp(rng.normal(1.0, 0.4, size=n))
+    lam = np.array([0.0, 0.35, 1.0])
+    out = ctx.eval_batch(coords, y, X, np.array([[phiX, 1.5, nug, phiR, phiA]]), lam)
+    assert out["status"][0] == 0
+    L = np.linalg.cholesky(V)
+    logdet = 2.0 * np.log(np.diag(L)).sum()
+    assert out["logdetV"][0] == pytest.approx(logdet, rel=1e-10)
+    Vi = lambda B: np.linalg.solve(L.T, np.linalg.solve(L, B))
+    for m, l in enumerate(lam):
+        yp = np.log(y) if l == 0 else (y ** l - 1) / l
+        beta = np.linalg.solve(X.T @ Vi(X), X.T @ Vi(yp))
+        r = yp - X @ beta
+        q = r @ Vi(r)
+        m2l = n * np.log(q / n) + logdet - 2 * (l - 1) * np.log(y).sum() + n * np.log(2 * np.pi) + n
+        assert -2 * out["loglik"][0, m] == pytest.approx(m2l, rel=1e-10)
+        np.testing.assert_allclose(out["betahat"][0, m], beta, rtol=1e-8, atol=1e-10)
+        assert out["sigma2hat"][0, m] == pytest.approx(q / n, rel=1e-9)
