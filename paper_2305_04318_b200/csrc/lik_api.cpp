@@ -45,6 +45,11 @@ struct lik_ctx {
   char* io = nullptr;
   size_t io_bytes = 0;
   int wave_points = 0;
+  // free-memory query of the last call (cudaMemGetInfo costs 0.1-5 ms of host time):
+  // a call with the same K and slot size reuses it, so it gets the same wave size
+  // and the workspace it already holds
+  size_t avail_cache = 0, avail_slot = 0;
+  int avail_K = -1;
   // timing
   double stage_ms[LIK_NSTAGES] = {0, 0, 0, 0};
   long long stage_n[LIK_NSTAGES] = {0, 0, 0, 0};
@@ -232,9 +237,17 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   // lik_set_wave_points overrides (85 % cap).
   int W;
   {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    const size_t avail = fr + c->ws_bytes;
+    size_t avail;
+    if (c->avail_K == K && c->avail_slot == slot_bytes) {
+      avail = c->avail_cache;
+    } else {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      avail = fr + c->ws_bytes;
+      c->avail_cache = avail;
+      c->avail_slot = slot_bytes;
+      c->avail_K = K;
+    }
     const size_t cap = (size_t)(0.85 * (double)avail) / slot_bytes;
     if (cap < 1) return fail(c, LIK_ENOMEM, "one workspace slot (%zu bytes) exceeds free HBM", slot_bytes);
     if (c->wave_points > 0) {
@@ -253,7 +266,10 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   }
   tr.mark("memgetinfo");
   int rc;
-  if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes))) return rc;
+  if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes))) {
+    c->avail_K = -1;  // query the free memory again next time
+    return rc;
+  }
   size_t pcb = c->pc_cap * sizeof(PointConst);
   if ((rc = ensure(c, &c->pc, &pcb, (size_t)K * sizeof(PointConst)))) return rc;
   c->pc_cap = pcb / sizeof(PointConst);

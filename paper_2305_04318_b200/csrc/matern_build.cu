@@ -165,6 +165,22 @@ cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaSt
   return cudaGetLastError();
 }
 
+// Monomial coefficients of the Chebyshev polynomials: kTco.v[j·N + k] = coefficient
+// of t^k in T_j (T_0 = 1, T_1 = t, T_j = 2t T_{j−1} − T_{j−2}); integers, exact in FP64.
+struct TcoTable {
+  double v[CHEB_N * CHEB_N];
+};
+constexpr TcoTable make_tco() {
+  TcoTable t{};
+  t.v[0] = 1.0;
+  t.v[CHEB_N + 1] = 1.0;
+  for (int jj = 2; jj < CHEB_N; ++jj)
+    for (int kk = 0; kk < CHEB_N; ++kk)
+      t.v[jj * CHEB_N + kk] = (kk > 0 ? 2.0 * t.v[(jj - 1) * CHEB_N + kk - 1] : 0.0) - t.v[(jj - 2) * CHEB_N + kk];
+  return t;
+}
+__device__ const TcoTable kTco = make_tco();
+
 // ---------------------------------------------------------------------------
 // table: one block per point of the wave.  ln ρ is evaluated exactly (Temme /
 // CF2 + recurrence) at the octave edges and at CHEB_N Chebyshev nodes of every
@@ -185,6 +201,12 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   __shared__ double f[CHEB_NOCT * CHEB_N];
   __shared__ double edge[CHEB_NOCT + 1];
   __shared__ int ez;
+  __shared__ double tco[CHEB_N * CHEB_N];   // tco[j][k] = coefficient of t^k in T_j
+  __shared__ double cosm[CHEB_N * CHEB_N];  // cosm[j][i] = cos(π j (i + ½) / N), the DCT-II matrix
+  for (int e = tid; e < CHEB_N * CHEB_N; e += 256) {
+    tco[e] = kTco.v[e];
+    cosm[e] = cospi((e / CHEB_N) * ((e % CHEB_N) + 0.5) / CHEB_N);
+  }
   // This point's s = 8κ·|Q h|² lies in [8κ·d²min/φ²max, 8κ·d²max/φ²min] (the singular
   // values of the anisotropy map Q are 1/φX, 1/φY): only those octaves, widened by
   // one on each side against rounding, are built; the build sends anything outside
@@ -225,21 +247,11 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   // Chebyshev coefficients of g (DCT-II), then monomial coefficients in t (T_j has
   // integer coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
   __shared__ double cheb[CHEB_NOCT * CHEB_N];
-  __shared__ double tco[CHEB_N * CHEB_N];  // tco[j][k] = coefficient of t^k in T_j
-  if (tid == 0) {
-    for (int e = 0; e < CHEB_N * CHEB_N; ++e) tco[e] = 0.0;
-    tco[0] = 1.0;
-    tco[CHEB_N + 1] = 1.0;
-    for (int jj = 2; jj < CHEB_N; ++jj)
-      for (int kk = 0; kk < CHEB_N; ++kk)
-        tco[jj * CHEB_N + kk] = (kk > 0 ? 2.0 * tco[(jj - 1) * CHEB_N + kk - 1] : 0.0) -
-                                tco[(jj - 2) * CHEB_N + kk];
-  }
   for (int idx = olo * CHEB_N + tid; idx < (ohi + 1) * CHEB_N; idx += 256) {
     const int o = idx / CHEB_N, jj = idx % CHEB_N;
     double cc = 0.0;
     if (CHEB_ELO + o < ez) {
-      for (int ii = 0; ii < CHEB_N; ++ii) cc += f[o * CHEB_N + ii] * cospi(jj * (ii + 0.5) / CHEB_N);
+      for (int ii = 0; ii < CHEB_N; ++ii) cc += f[o * CHEB_N + ii] * cosm[jj * CHEB_N + ii];
       cc *= (jj == 0 ? 1.0 : 2.0) / CHEB_N;
     }
     cheb[idx] = cc;
