@@ -467,7 +467,7 @@ static_assert(PW == 8 || PW == 16, "panel width");
 // dependent chain is two ops per step).  Only the pivot chain is serial; it uses no
 // divisions (the FP64 pipe is shared with the co-resident CTA's DMMAs, so every
 // dependent FP64 op on it is slow).  Pivots ≥ vloc are skipped (their rows and
-// columns of D_p⁻¹ are 0).  dlog[c0 + c] = log(pivot_c); a pivot ≤ tol sets flag[0].
+// columns of D_p⁻¹ are 0).  dlog[c0 + c] = pivot_c (pivots_to_log takes the logs); a pivot ≤ tol sets flag[0].
 __device__ __forceinline__ void factor_block(double* S, double* X, int c0, int vloc, double tol,
                                              double* dlog, int* flag) {
   const int lane = threadIdx.x & 31, l = lane & (PW - 1);
@@ -498,7 +498,7 @@ __device__ __forceinline__ void factor_block(double* S, double* X, int c0, int v
       }
     }
   }
-  if (lane < PW && l < vloc) dlog[c0 + l] = log(my_piv);
+  if (lane < PW && l < vloc) dlog[c0 + l] = my_piv;  // log taken later, off the lead warp (pivots_to_log)
   double x[PW];
 #pragma unroll
   for (int i = 0; i < PW; ++i) x[i] = (i == l && l < vloc) ? 1.0 : 0.0;
@@ -576,6 +576,13 @@ __device__ void panel_update(double* S, const double* X, int c0) {  // (b) then 
   __syncthreads();
 }
 
+// dlog[c] = log(pivot_c) for c < v, by threads 0..v−1 (the lead warp, whose serial
+// chain gates every panel, stores the raw pivots); visible after the caller's next
+// __syncthreads.
+__device__ __forceinline__ void pivots_to_log(double* dlog, int v) {
+  if ((int)threadIdx.x < v) dlog[threadIdx.x] = log(dlog[threadIdx.x]);
+}
+
 // Blocked Cholesky + inverse of a 64×64 tile in shared memory (lower part used)
 // whose rows/columns ≥ v are the identity padding of V.  64/PW panels:
 //   (a) the lead warp factors the PW×PW diagonal block D_p and inverts it into X
@@ -636,6 +643,7 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     const int i = e >> 6, c = e & 63;
     if (c / PW > i / PW) X[sw_off(i, c)] = 0.0;
   }
+  pivots_to_log(dlog, v);
   __syncthreads();
   if (PW == 8) {  // level 8 → 16: X_{(2g+1),(2g)} = −X_{(2g+1),(2g+1)} (L_{(2g+1),(2g)} X_{(2g),(2g)})
     const int lr = lane >> 2, lc = lane & 3, o = 16 * warp;
@@ -725,6 +733,8 @@ __device__ int potrf_tail(double* S, int v, double tol, double* dlog, int* flag,
     if (flag[0]) return 1;
     if (c0 + PW < TB) panel_update(S, X, c0);
   }
+  pivots_to_log(dlog, v);
+  __syncthreads();
   return 0;
 }
 
