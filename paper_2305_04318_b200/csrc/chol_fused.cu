@@ -529,28 +529,36 @@ __device__ __forceinline__ void factor_block(double* S, double* X, int c0, int v
 //       of [c0+PW, 64)², one warp per tile.
 // DMMA fragments (m8n8k4): a = A[r + lane/4][k + lane%4], b = B[k + lane%4][n + lane/4],
 // c = C[r + lane/4][n + 2(lane%4) + {0,1}].
-__device__ __forceinline__ void panel_product(double* S, const double* X, int c0) {  // (b)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lr = lane >> 2, lc = lane & 3;
-  const int b0 = c0 + PW, rt = (TB - b0) >> 3;
-  if (warp < rt) {
-    const int r = b0 + 8 * warp;
-    double c[PW / 8][2];
+// One 8-row tile (rows b0 + 8·rtile, b0 = c0 + PW) of step (b), in place.
+__device__ __forceinline__ void panel_tile(double* S, const double* X, int c0, int rtile) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  const int r = c0 + PW + 8 * rtile;
+  double c[PW / 8][2];
 #pragma unroll
-    for (int nt = 0; nt < PW / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  for (int nt = 0; nt < PW / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
 #pragma unroll
-    for (int ks = 0; ks < PW / 4; ++ks) {
-      const double a = S[sw_off(r + lr, c0 + 4 * ks + lc)];
+  for (int ks = 0; ks < PW / 4; ++ks) {
+    const double a = S[sw_off(r + lr, c0 + 4 * ks + lc)];
 #pragma unroll
-      for (int nt = 0; nt < PW / 8; ++nt) {
-        if (4 * ks > 8 * nt + 7) continue;  // D_p⁻¹ is lower triangular
-        dmma(c[nt], a, X[sw_off(c0 + 8 * nt + lr, c0 + 4 * ks + lc)]);
-      }
+    for (int nt = 0; nt < PW / 8; ++nt) {
+      if (4 * ks > 8 * nt + 7) continue;  // D_p⁻¹ is lower triangular
+      dmma(c[nt], a, X[sw_off(c0 + 8 * nt + lr, c0 + 4 * ks + lc)]);
     }
-#pragma unroll
-    for (int nt = 0; nt < PW / 8; ++nt)
-      *reinterpret_cast<double2*>(S + sw_off(r + lr, c0 + 8 * nt + 2 * lc)) = make_double2(c[nt][0], c[nt][1]);
   }
+#pragma unroll
+  for (int nt = 0; nt < PW / 8; ++nt)
+    *reinterpret_cast<double2*>(S + sw_off(r + lr, c0 + 8 * nt + 2 * lc)) = make_double2(c[nt][0], c[nt][1]);
 }
+
+__device__ __forceinline__ void panel_product(double* S, const double* X, int c0) {  // (b)
+  const int warp = threadIdx.x >> 5, rt = (TB - c0 - PW) >> 3;
+  if (warp < rt) panel_tile(S, X, c0, warp);
+}
+
+// Named barrier 1 (barrier 0 is __syncthreads): the lead warp arrives after its
+// shared-memory stores, the other warps wait there (all NT threads counted).
+__device__ __forceinline__ void named_arrive1() { asm volatile("bar.arrive 1, %0;\n" ::"n"(NT) : "memory"); }
+__device__ __forceinline__ void named_sync1() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory"); }
 
 // (c) for tile t of the lower triangle of [c0+PW, 64)² in 8×8 tiles (t = 0: the
 // next diagonal block).
@@ -621,10 +629,31 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
   if (flag[0]) return 1;
 #endif
   for (int c0 = 0; c0 + PW < TB; c0 += PW) {
+    const int rt = (TB - c0 - PW) >> 3, ntile = rt * (rt + 1) / 2;
+    constexpr int NR = PW / 8;                        // row tiles of the next diagonal block
+    constexpr int ND = (PW / 8) * (PW / 8 + 1) / 2;  // trailing tiles of the next diagonal block
+#ifndef LIK_POTRF_TWO_BARRIERS
+    // One CTA barrier per panel: the lead warp computes the panel product of the next
+    // diagonal block's rows itself (their inputs were final at the previous barrier),
+    // signals the other warps through named barrier 1, updates and factors that
+    // block; the other warps compute the remaining rows, wait for the lead's rows at
+    // barrier 1 (only the trailing tiles below the next block read them) and update
+    // the rest of the trailing matrix.
+    if (warp == LEAD_WARP) {
+      for (int q = 0; q < NR; ++q) panel_tile(S, X, c0, q);
+      __syncwarp();
+      named_arrive1();
+      for (int t = 0; t < ND; ++t) trailing_tile(S, c0, t);
+      __syncwarp();
+      factor_block(S, X, c0 + PW, PW, tol, dlog, flag);
+    } else {
+      for (int q = NR + warp; q < rt; q += NT / 32 - 1) panel_tile(S, X, c0, q);
+      named_sync1();
+      for (int t = ND + warp; t < ntile; t += NT / 32 - 1) trailing_tile(S, c0, t);
+    }
+#else
     panel_product(S, X, c0);
     __syncthreads();
-    const int rt = (TB - c0 - PW) >> 3, ntile = rt * (rt + 1) / 2;
-    constexpr int ND = (PW / 8) * (PW / 8 + 1) / 2;  // trailing tiles of the next diagonal block
     if (warp == LEAD_WARP) {
       for (int t = 0; t < ND; ++t) trailing_tile(S, c0, t);
       __syncwarp();
@@ -632,6 +661,7 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     } else {
       for (int t = ND + warp; t < ntile; t += NT / 32 - 1) trailing_tile(S, c0, t);
     }
+#endif
     __syncthreads();
     SUB(13);
 #ifndef LIK_EXP_SAMESRC
