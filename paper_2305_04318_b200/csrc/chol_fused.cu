@@ -386,9 +386,13 @@ struct Src {
 // stage's previous round (the ring runs on across k-loops: pp.seq counts chunks).
 // At the start of chunk q one warp (rotating) refills the stage of chunk q−1 with
 // chunk q−1+NSTAGE; the first NSTAGE chunks are issued by the lead thread.
-__device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
-                                      bool mine_b, int rbase, int mlim, int nlim, int lane,
-                                      const double* slot_lo, const double* slot_hi) {
+// MODE: the chunk product, fixed for the whole k-loop — 0 all rows and column
+// groups, 2/4/6 a diagonal tile's first column groups, 1 a partly filled row block,
+// 9 no rows (the warp still takes part in the stage protocol); −1 decides per chunk.
+template <int MODE>
+__device__ __forceinline__ void kloop_m(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
+                                        bool mine_b, int rbase, int mlim, int nlim, int lane,
+                                        const double* slot_lo, const double* slot_hi) {
   const int tid = threadIdx.x;
   const uint32_t seq = pp.seq;
   auto copy = [&](double* dst, const Src& sr, int q, uint32_t bar, uint64_t pol) {
@@ -442,11 +446,46 @@ __device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B,
     if (tid == 224) atomicAdd(&g_lik_phase[q == 0 ? 9 : 15], (unsigned long long)(clock64() - tw0));
 #endif
     const double* st = pp.stages + s * STAGE_D;
-    mma_chunk_any(acc, st + (mine_b ? CHUNK_D : 0), rbase, mlim, nlim, st + 2 * CHUNK_D, lane);
+    const double* Ab = st + (mine_b ? CHUNK_D : 0);
+    if constexpr (MODE == -1) mma_chunk_any(acc, Ab, rbase, mlim, nlim, st + 2 * CHUNK_D, lane);
+    else if constexpr (MODE == 0) mma_chunk<true>(acc, Ab, rbase, MI, st + 2 * CHUNK_D, lane);
+    else if constexpr (MODE == 2 || MODE == 4 || MODE == 6)
+      mma_chunk<true, MODE>(acc, Ab, rbase, MI, st + 2 * CHUNK_D, lane);
+    else if constexpr (MODE == 1) mma_chunk<false>(acc, Ab, rbase, mlim, st + 2 * CHUNK_D, lane);
     __syncwarp();
-    if (lane == 0) mbar_arrive(saddr(&pp.empty[s]));
+    // The release must not overtake this warp's shared-memory loads of the stage:
+    // the DMMAs consuming them may be scheduled after the arrive, and
+    // mbarrier.arrive.release alone was measured not to hold back loads still in
+    // flight — the producer's next bulk copy then overwrote a stage being read
+    // (run-to-run differences at ~0.5 % of the points with the full-tile loop
+    // specialised; this was also the v13 race).  The CTA fence waits for them.
+    if (lane == 0) {
+      __threadfence_block();
+      mbar_arrive(saddr(&pp.empty[s]));
+    }
   }
   pp.seq = seq + nq;
+}
+
+// Which chunk products get a k-loop of their own (no per-chunk dispatch): bit 0 full
+// tiles (the default: +0.8 % at C4), bit 1 partial row blocks, bit 2 diagonal tiles,
+// bit 3 rowless warps; the rest dispatch per chunk (mma_chunk_any).
+#ifndef LIK_KLOOP_TMPL_MASK
+#define LIK_KLOOP_TMPL_MASK 1
+#endif
+__device__ __forceinline__ void kloop(Acc& acc, Pipe& pp, Src A0, Src A1, Src B, int nq,
+                                      bool mine_b, int rbase, int mlim, int nlim, int lane,
+                                      const double* slot_lo, const double* slot_hi) {
+#define KL(M) kloop_m<M>(acc, pp, A0, A1, B, nq, mine_b, rbase, mlim, nlim, lane, slot_lo, slot_hi)
+  constexpr int TM = LIK_KLOOP_TMPL_MASK;
+  if (mlim == MI && nlim == NI && (TM & 1)) KL(0);
+  else if (mlim == MI && nlim == 2 && (TM & 4)) KL(2);
+  else if (mlim == MI && nlim == 4 && (TM & 4)) KL(4);
+  else if (mlim == MI && nlim == 6 && (TM & 4)) KL(6);
+  else if (mlim > 0 && mlim < MI && (TM & 2)) KL(1);
+  else if (mlim == 0 && (TM & 8)) KL(9);
+  else KL(-1);
+#undef KL
 }
 
 // 32×32 scratch (T): two swizzled 32×16 halves, the chunk layout's bank pattern.
@@ -924,6 +963,11 @@ __global__ void LIK_CHOL_BOUNDS chol_fused_kernel(CholArgs A) {
             logdet += s;
           }
           PH(4);
+          // The staging tile and scratch alias the stage ring, and the next row
+          // block's first chunks are written there by bulk copies (async proxy):
+          // order this column's generic stores to them before those copies (a CTA
+          // barrier alone does not order the two proxies).
+          fence_proxy_async();
           __syncthreads();  // L_jj⁻¹ complete; the ring's memory is free again
           PH(5);
         }
