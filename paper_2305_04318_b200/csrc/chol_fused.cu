@@ -681,6 +681,7 @@ __device__ int potrf_inv64(double* S, int v, double tol, double* dlog, int* flag
     if (warp == LEAD_WARP) {
       for (int q = 0; q < NR; ++q) panel_tile(S, X, c0, q);
       __syncwarp();
+      __threadfence_block();  // the stores complete before the non-blocking arrive (cf. kloop)
       named_arrive1();
       for (int t = 0; t < ND; ++t) trailing_tile(S, c0, t);
       __syncwarp();
