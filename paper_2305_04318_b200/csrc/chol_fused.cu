@@ -515,10 +515,11 @@ __device__ __forceinline__ void factor_block(double* S, double* X, int c0, int v
   for (int k = 0; k < PW; ++k) a[k] = (k <= l) ? S[sw_off(c0 + l, c0 + k)] : 0.0;
   int bad = 0;
   double my_piv = 1.0, my_rinv = 1.0;
+  double piv_next = __shfl_sync(0xffffffffu, a[0], 0);
 #pragma unroll
   for (int c = 0; c < PW; ++c) {
     if (c < vloc) {
-      const double piv = __shfl_sync(0xffffffffu, a[c], c);
+      const double piv = piv_next;
       bad |= !(piv > tol);
       const double rinv = rsqrt(piv);
       if (l == c) {
@@ -527,6 +528,12 @@ __device__ __forceinline__ void factor_block(double* S, double* X, int c0, int v
         my_rinv = rinv;
       } else if (l > c) {
         a[c] *= rinv;
+      }
+      // the next pivot from lane c+1's own registers (the same FMA as its update
+      // below), broadcast once: the serial chain waits for one shuffle per pivot
+      if (c + 1 < PW) {
+        const double pn = a[c + 1] - a[c] * a[c];
+        piv_next = __shfl_sync(0xffffffffu, pn, c + 1);
       }
 #pragma unroll
       for (int k = 0; k < PW; ++k) {  // constant trip count: a[] stays in registers
