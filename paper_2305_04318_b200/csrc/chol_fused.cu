@@ -28,6 +28,14 @@
 // CTAs per SM (≤ 128 registers, ~105 KB shared memory each), so the serial
 // phases of one point (diagonal factorisation, inverse) overlap the DMMA phases
 // of the other.
+//
+// Ordering rules of the stage protocol (each one was needed):
+// a warp releases a stage (empty mbarrier arrive) only after a CTA fence, so its
+// shared-memory loads of the stage have completed before the producer's next bulk
+// copy overwrites it; generic stores into ring memory (the staging tile) and into
+// L tiles later read by bulk copies are followed by fence.proxy.async before the
+// barrier that precedes those copies; mbarrier phases are waited by parity, which
+// is safe because no warp can run more than one phase ahead of a stage.
 #include <cfloat>
 #include <cstdint>
 #include <cstdio>
