@@ -241,14 +241,22 @@ def test_shard_assembly_bitwise_vs_one_gpu(ctx, world):
         assert np.array_equal(table[key], full[key].cpu().numpy(), equal_nan=True), (world, key)
 
 
-@pytest.mark.parametrize("name, K, reps", [("C3", 1776, 3), ("C4", 1184, 2)])
+@pytest.mark.parametrize("name, K, reps", [("C3", 1776, 3), ("C4", 1184, 2), ("C2", 2960, 3),
+                                            ("n1020", 1776, 3)])
 def test_bitwise_repeatability_over_cta_rounds(ctx, name, K, reps):
     """Repeated calls give bitwise identical outputs with several rounds of resident
-    CTAs per launch (K = 6 resp. 4 × 296): CTAs that start on an SM after another
+    CTAs per launch (K = 6 resp. 4 / 10 × 296): CTAs that start on an SM after another
     finished see its shared memory and a different timing mix, which is where a
-    race in the k-loop's stage protocol showed up once (~0.1 % of the points,
-    DESIGN.md §5)."""
-    coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
+    race in the k-loop's stage protocol showed (a stage released before the warp's
+    loads of it completed; ~0.5 % of the points).  n = 1020 takes the
+    separate augmented tile row (no merged tail); C2 is diagonal-factorisation bound."""
+    if name == "n1020":
+        base = synthgen.CONFIGS["C3"]
+        cfg = synthgen.Config("n1020", 1020, base.p, K, base.M, base.iso, base.layout, "n1020")
+        coords, y, X = synthgen.make_dataset(cfg, seed=7)
+        P, lam = synthgen.make_params(cfg, K, seed=8), synthgen.make_lambdas(cfg.M)
+    else:
+        coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
     t = [torch.tensor(v, device="cuda") for v in (coords, y, X, P, lam)]
     first = {k: v.cpu().numpy() for k, v in ctx.eval_batch_device(*t).items()}
     for _ in range(reps):
