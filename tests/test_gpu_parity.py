@@ -388,8 +388,8 @@ def test_bounds_checked_build():
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     lib_b = os.path.join(root, "paper_2305_04318_b200", "liblik_bounds.so")
-    if not os.path.exists(lib_b):
-        from paper_2305_04318_b200 import build as b
+    from paper_2305_04318_b200 import build as b
+    if b._stale(lib_b):  # rebuilt whenever a source is newer (a stale variant would test old code)
         b.build(force=True, defines=("LIK_BOUNDS_CHECK",), out=lib_b)
     env = dict(os.environ, LIK_LIBRARY=lib_b)
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "debug", "sanitize_case.py")], cwd=root,
