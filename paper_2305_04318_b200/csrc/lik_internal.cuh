@@ -97,16 +97,26 @@ struct PointConst {
 
 // Per-point Chebyshev table of ln ρ on binary octaves of s = z² = 8κ·d² ∈ [2^e,
 // 2^{e+1}), e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1 (the build needs no square
-// root).  Each octave stores CHEB_STRIDE doubles: a base H_o, one pad (so the
-// coefficients are 16-byte aligned), then the CHEB_N monomial coefficients (in
-// t = s/2^e·2 − 3 ∈ [−1, 1)) of the degree-19 Chebyshev interpolant of
-// h(s) = ln ρ(√s) − H_o, so that ln ρ = H_o + h(s).  Below 2^CHEB_ELO the exact
-// evaluation is used; at and above 2^e_zero ρ = 0.
-constexpr int CHEB_N = 20;
+// root).  Each interval (CHEB_SUB per octave) stores CHEB_STRIDE doubles: a base
+// H, one pad (so the coefficients are 16-byte aligned), then the CHEB_N monomial
+// coefficients (in t ∈ [−1, 1), an exact power-of-two map of s) of the degree
+// CHEB_N − 1 Chebyshev interpolant of h(s) = ln ρ(√s) − H, so that ln ρ = H + h(s).
+// Below 2^CHEB_ELO the exact evaluation is used; at and above 2^e_zero ρ = 0.
+// LIK_CHEB_SUB = 2 splits every octave at its linear midpoint ([1, 1.5) and
+// [1.5, 2) × 2^e; interval = SUB·octave + the top mantissa bit of s) with degree 15
+// instead of 19: the worse half sees the branch point at s = 0 from 5 half-widths
+// (Bernstein ρ = 9.9 vs 5.8), so the truncation stays at the same ~1e-16 level.
+#ifndef LIK_CHEB_SUB
+#define LIK_CHEB_SUB 2
+#endif
+constexpr int CHEB_SUB = LIK_CHEB_SUB;
+static_assert(CHEB_SUB == 1 || CHEB_SUB == 2, "intervals per octave");
+constexpr int CHEB_N = CHEB_SUB == 1 ? 20 : 16;
 constexpr int CHEB_STRIDE = CHEB_N + 2;
 constexpr int CHEB_ELO = -52;
 constexpr int CHEB_NOCT = 80;
-constexpr int TABLE_D = CHEB_STRIDE * CHEB_NOCT;
+constexpr int CHEB_NINT = CHEB_NOCT * CHEB_SUB;  // intervals
+constexpr int TABLE_D = CHEB_STRIDE * CHEB_NINT;
 
 // Launch wrappers (defined in the .cu files).  All enqueue on `st`.
 // prep: Box-Cox rows of Bᵀ, S = Σ log y, and the site gather coords_p[i] = coords[perm[i]]

@@ -183,12 +183,13 @@ __device__ const TcoTable kTco = make_tco();
 
 // ---------------------------------------------------------------------------
 // table: one block per point of the wave.  ln ρ is evaluated exactly (Temme /
-// CF2 + recurrence) at the octave edges and at CHEB_N Chebyshev nodes of every
-// binary octave of s = z² below the underflow octave e_zero, detrended by the line
-// through the edge values (so the DCT works on a small function) and turned into
-// Chebyshev coefficients (DCT-II), then monomial ones with the line added back.
-// ln ρ(√s) is analytic on each octave [a, 2a] (its only finite singularity is the
-// branch point s = 0, three half-widths from the centre), so degree 19 reaches the
+// CF2 + recurrence) at the interval edges and at CHEB_N Chebyshev nodes of every
+// interval (CHEB_SUB per binary octave of s = z²) below the underflow octave
+// e_zero, detrended by the line through the edge values (so the DCT works on a
+// small function) and turned into Chebyshev coefficients (DCT-II), then monomial
+// ones with the line added back.  ln ρ(√s) is analytic on each interval (its only
+// finite singularity is the branch point s = 0: 3 half-widths from the centre of
+// a whole octave, 5 from that of [1, 1.5)·2^e), so degree 19 resp. 15 reaches the
 // FP64 rounding floor (~1e-16·max(1, |ln ρ|)), DESIGN.md §5.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc, int k0,
@@ -198,8 +199,8 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   const int tid = threadIdx.x;
   const PointConst P = pc[k];
   if (P.mode != MODE_BESSEL) return;
-  __shared__ double f[CHEB_NOCT * CHEB_N];
-  __shared__ double edge[CHEB_NOCT + 1];
+  __shared__ double f[CHEB_NINT * CHEB_N];
+  __shared__ double edge[CHEB_NINT + 1];
   __shared__ int ez;
   __shared__ double tco[CHEB_N * CHEB_N];   // tco[j][k] = coefficient of t^k in T_j
   __shared__ double cosm[CHEB_N * CHEB_N];  // cosm[j][i] = cos(π j (i + ½) / N), the DCT-II matrix
@@ -216,12 +217,14 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   const double s_lo = P.eightk * dstat[0] * q_lo, s_hi = P.eightk * dstat[1] * q_hi;
   const int olo = s_lo > 0.0 ? max(0, min(CHEB_NOCT - 1, ilogb(s_lo) - CHEB_ELO - 1)) : 0;
   const int ohi = s_hi > 0.0 ? max(olo, min(CHEB_NOCT - 1, ilogb(s_hi) - CHEB_ELO + 1)) : olo;
-  for (int o = olo + tid; o <= ohi + 1; o += 256) edge[o] = log_rho_exact(P, sqrt(ldexp(1.0, CHEB_ELO + o)));
+  // interval edges: s = 2^(ELO + iv/SUB) · (1 + (iv mod SUB)/SUB)
+  for (int iv = olo * CHEB_SUB + tid; iv <= (ohi + 1) * CHEB_SUB; iv += 256)
+    edge[iv] = log_rho_exact(P, sqrt(ldexp(1.0 + (double)(iv % CHEB_SUB) / CHEB_SUB, CHEB_ELO + iv / CHEB_SUB)));
   __syncthreads();
   if (tid == 0) {
     int e0 = CHEB_ELO + CHEB_NOCT + 64;  // sentinel: never underflows inside the table range
     for (int o = olo; o <= ohi + 1; ++o)
-      if (edge[o] < -750.0) {
+      if (edge[o * CHEB_SUB] < -750.0) {
         e0 = CHEB_ELO + o;
         break;
       }
@@ -232,41 +235,42 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   }
   __syncthreads();
   // g = ln ρ(√s) − L_o(x) at the nodes, L_o the line through the octave's edge values
-  for (int idx = olo * CHEB_N + tid; idx < (ohi + 1) * CHEB_N; idx += 256) {
-    const int o = idx / CHEB_N, i = idx % CHEB_N;
-    const int e = CHEB_ELO + o;
+  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
+    const int iv = idx / CHEB_N, i = idx % CHEB_N;  // interval iv: octave iv/SUB, part iv mod SUB
+    const int e = CHEB_ELO + iv / CHEB_SUB;
     double v = 0.0;
     if (e < ez) {
       const double x = cospi((i + 0.5) / CHEB_N);
-      const double sn = ldexp(1.5 + 0.5 * x, e);
-      v = log_rho_exact(P, sqrt(sn)) - 0.5 * (edge[o] + edge[o + 1]) - 0.5 * (edge[o + 1] - edge[o]) * x;
+      const double lo = 1.0 + (double)(iv % CHEB_SUB) / CHEB_SUB, hw = 0.5 / CHEB_SUB;
+      const double sn = ldexp(lo + hw * (1.0 + x), e);
+      v = log_rho_exact(P, sqrt(sn)) - 0.5 * (edge[iv] + edge[iv + 1]) - 0.5 * (edge[iv + 1] - edge[iv]) * x;
     }
     f[idx] = v;
   }
   __syncthreads();
   // Chebyshev coefficients of g (DCT-II), then monomial coefficients in t (T_j has
   // integer coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
-  __shared__ double cheb[CHEB_NOCT * CHEB_N];
-  for (int idx = olo * CHEB_N + tid; idx < (ohi + 1) * CHEB_N; idx += 256) {
-    const int o = idx / CHEB_N, jj = idx % CHEB_N;
+  __shared__ double cheb[CHEB_NINT * CHEB_N];
+  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
+    const int iv = idx / CHEB_N, jj = idx % CHEB_N;
     double cc = 0.0;
-    if (CHEB_ELO + o < ez) {
-      for (int ii = 0; ii < CHEB_N; ++ii) cc += f[o * CHEB_N + ii] * cosm[jj * CHEB_N + ii];
+    if (CHEB_ELO + iv / CHEB_SUB < ez) {
+      for (int ii = 0; ii < CHEB_N; ++ii) cc += f[iv * CHEB_N + ii] * cosm[jj * CHEB_N + ii];
       cc *= (jj == 0 ? 1.0 : 2.0) / CHEB_N;
     }
     cheb[idx] = cc;
   }
   __syncthreads();
   double* T = table + (size_t)blockIdx.x * TABLE_D;
-  for (int idx = olo * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_STRIDE; idx += 256) {
-    const int o = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 2;
+  for (int idx = olo * CHEB_SUB * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_STRIDE; idx += 256) {
+    const int iv = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 2;
     double a = 0.0;
-    if (CHEB_ELO + o < ez) {
+    if (CHEB_ELO + iv / CHEB_SUB < ez) {
       if (kk == -2) {
-        a = 0.5 * (edge[o] + edge[o + 1]);  // H_o: the line's value at t = 0
+        a = 0.5 * (edge[iv] + edge[iv + 1]);  // H: the line's value at t = 0
       } else if (kk >= 0) {
-        for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[o * CHEB_N + jj] * tco[jj * CHEB_N + kk];
-        if (kk == 1) a += 0.5 * (edge[o + 1] - edge[o]);  // the line's slope in t
+        for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[iv * CHEB_N + jj] * tco[jj * CHEB_N + kk];
+        if (kk == 1) a += 0.5 * (edge[iv + 1] - edge[iv]);  // the line's slope in t
       }
     }
     T[idx] = a;
@@ -311,7 +315,8 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
   if (P.mode == MODE_BESSEL) {
     const double* src = table + (size_t)slot * TABLE_D;
     const int oend = min(P.ohi + 1, max(P.olo, P.e_zero - CHEB_ELO));  // octaves [olo, oend)
-    for (int e = P.olo * CHEB_STRIDE + threadIdx.x; e < oend * CHEB_STRIDE; e += 256) coef[e] = src[e];
+    for (int e = P.olo * CHEB_SUB * CHEB_STRIDE + threadIdx.x; e < oend * CHEB_SUB * CHEB_STRIDE; e += 256)
+      coef[e] = src[e];
   }
   // thread -> column c, rows r0 + 4q (q < 16): a warp covers 32 consecutive
   // columns of one row; with Morton-ordered sites their z values mostly share an
