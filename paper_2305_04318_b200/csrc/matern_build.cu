@@ -290,7 +290,10 @@ cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, const do
 // written as 0).  Padded rows/columns (index ≥ n) hold the identity, which
 // leaves log|V| and L⁻¹B unchanged.  Augmented tile j holds Bᵀ[:, 64j:64j+64].
 // ---------------------------------------------------------------------------
-constexpr int BUILD_TILES = 4;  // tiles of one point per block (amortises the table load)
+#ifndef LIK_BUILD_TILES
+#define LIK_BUILD_TILES 8
+#endif
+constexpr int BUILD_TILES = LIK_BUILD_TILES;  // tiles of one point per block (amortises the table load)
 #ifndef LIK_BUILD_NE
 #define LIK_BUILD_NE 4  // 4: 35.4 ms, 2: 36.1 ms per 2,960 C4 points
 #endif
