@@ -312,8 +312,8 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   for (int w = 0; w < nwaves; ++w) {
     const int k0 = w * W, kw = std::min(W, K - k0);
-    CUDA_TRY(c, lik::launch_table(c->pc, k0, kw, c->table, S + 1, st));
-    CUDA_TRY(c, lik::launch_build(coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
+    CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, k0, kw, c->table, S + 1, st));
+    CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
     a.ws = c->ws;
@@ -670,8 +670,8 @@ int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const doub
   if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));
   CUDA_TRY(c, lik::launch_dist_range(coords, n, c->S + 1, st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
-  CUDA_TRY(c, lik::launch_table(c->pc, 0, K, c->table, c->S + 1, st));
-  CUDA_TRY(c, lik::launch_build(coords, g, c->pc, 0, K, c->table, nullptr, c->ws, st));
+  CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, 0, K, c->table, c->S + 1, st));
+  CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords, g, c->pc, 0, K, c->table, nullptr, c->ws, st));
   CUDA_TRY(c, lik::launch_unpack_V(g, c->pc, K, c->ws, V, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
   return LIK_OK;

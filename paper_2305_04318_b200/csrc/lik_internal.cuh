@@ -102,21 +102,28 @@ struct PointConst {
 // coefficients (in t ∈ [−1, 1), an exact power-of-two map of s) of the degree
 // CHEB_N − 1 Chebyshev interpolant of h(s) = ln ρ(√s) − H, so that ln ρ = H + h(s).
 // Below 2^CHEB_ELO the exact evaluation is used; at and above 2^e_zero ρ = 0.
-// LIK_CHEB_SUB = 2 splits every octave at its linear midpoint ([1, 1.5) and
-// [1.5, 2) × 2^e; interval = SUB·octave + the top mantissa bit of s) with degree 15
-// instead of 19: the worse half sees the branch point at s = 0 from 5 half-widths
-// (Bernstein ρ = 9.9 vs 5.8), so the truncation stays at the same ~1e-16 level.
-#ifndef LIK_CHEB_SUB
-#define LIK_CHEB_SUB 2
-#endif
-constexpr int CHEB_SUB = LIK_CHEB_SUB;
-static_assert(CHEB_SUB == 1 || CHEB_SUB == 2, "intervals per octave");
-constexpr int CHEB_N = CHEB_SUB == 1 ? 20 : 16;
-constexpr int CHEB_STRIDE = CHEB_N + 2;
+// Two table layouts, chosen per call from n (cheb_sub_for): SUB = 1 whole octaves
+// with degree 19; SUB = 2 splits every octave at its linear midpoint ([1, 1.5) and
+// [1.5, 2) × 2^e; interval = SUB·octave + the top mantissa bit of s) with degree
+// 15 — the worse half sees the branch point at s = 0 from 5 half-widths (Bernstein
+// ρ = 9.9 vs 5.8), so the truncation stays at the same ~1e-16 level.  Halves cost
+// the table kernel 1.6× the exact evaluations per point and save the build 4 DFMA
+// and 2 LDS.128 per element, so they pay from a few hundred sites on.
 constexpr int CHEB_ELO = -52;
 constexpr int CHEB_NOCT = 80;
-constexpr int CHEB_NINT = CHEB_NOCT * CHEB_SUB;  // intervals
-constexpr int TABLE_D = CHEB_STRIDE * CHEB_NINT;
+template <int SUB>
+struct Cheb {
+  static_assert(SUB == 1 || SUB == 2, "intervals per octave");
+  static constexpr int N = SUB == 1 ? 20 : 16;  // coefficients per interval
+  static constexpr int STRIDE = N + 2;
+  static constexpr int NINT = CHEB_NOCT * SUB;  // intervals
+  static constexpr int TABLE_D = STRIDE * NINT;
+};
+constexpr int TABLE_D = Cheb<1>::TABLE_D > Cheb<2>::TABLE_D ? Cheb<1>::TABLE_D : Cheb<2>::TABLE_D;
+#ifndef LIK_CHEB_SUB_MIN_N
+#define LIK_CHEB_SUB_MIN_N 256
+#endif
+inline int cheb_sub_for(int n) { return n >= LIK_CHEB_SUB_MIN_N ? 2 : 1; }
 
 // Launch wrappers (defined in the .cu files).  All enqueue on `st`.
 // prep: Box-Cox rows of Bᵀ, S = Σ log y, and the site gather coords_p[i] = coords[perm[i]]
@@ -128,9 +135,9 @@ cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream
 // dist_range: dstat[0] = min, dstat[1] = max squared Euclidean distance over the
 // site pairs (bounds each point's range of s = z² for the table).
 cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st);
-cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, const double* dstat,
+cudaError_t launch_table(int sub, PointConst* pc, int k0, int kw, double* table, const double* dstat,
                          cudaStream_t st);
-cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
+cudaError_t launch_build(int sub, const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
                          int kw, const double* table, const double* Bt, double* ws,
                          cudaStream_t st);
 cudaError_t launch_unpack_V(const SlotGeom& g, const PointConst* pc, int kw, const double* ws,

@@ -167,19 +167,22 @@ cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaSt
 
 // Monomial coefficients of the Chebyshev polynomials: kTco.v[j·N + k] = coefficient
 // of t^k in T_j (T_0 = 1, T_1 = t, T_j = 2t T_{j−1} − T_{j−2}); integers, exact in FP64.
+template <int N>
 struct TcoTable {
-  double v[CHEB_N * CHEB_N];
+  double v[N * N];
 };
-constexpr TcoTable make_tco() {
-  TcoTable t{};
+template <int N>
+constexpr TcoTable<N> make_tco() {
+  TcoTable<N> t{};
   t.v[0] = 1.0;
-  t.v[CHEB_N + 1] = 1.0;
-  for (int jj = 2; jj < CHEB_N; ++jj)
-    for (int kk = 0; kk < CHEB_N; ++kk)
-      t.v[jj * CHEB_N + kk] = (kk > 0 ? 2.0 * t.v[(jj - 1) * CHEB_N + kk - 1] : 0.0) - t.v[(jj - 2) * CHEB_N + kk];
+  t.v[N + 1] = 1.0;
+  for (int jj = 2; jj < N; ++jj)
+    for (int kk = 0; kk < N; ++kk)
+      t.v[jj * N + kk] = (kk > 0 ? 2.0 * t.v[(jj - 1) * N + kk - 1] : 0.0) - t.v[(jj - 2) * N + kk];
   return t;
 }
-__device__ const TcoTable kTco = make_tco();
+__device__ const TcoTable<Cheb<1>::N> kTco1 = make_tco<Cheb<1>::N>();
+__device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
 
 // ---------------------------------------------------------------------------
 // table: one block per point of the wave.  ln ρ is evaluated exactly (Temme /
@@ -192,9 +195,12 @@ __device__ const TcoTable kTco = make_tco();
 // a whole octave, 5 from that of [1, 1.5)·2^e), so degree 19 resp. 15 reaches the
 // FP64 rounding floor (~1e-16·max(1, |ln ρ|)), DESIGN.md §5.
 // ---------------------------------------------------------------------------
+template <int SUB>
 __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc, int k0,
                                                     double* __restrict__ table,
                                                     const double* __restrict__ dstat) {
+  constexpr int CHEB_SUB = SUB, CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
+  constexpr int CHEB_NINT = Cheb<SUB>::NINT, TABLE_D = Cheb<SUB>::TABLE_D;
   const int k = k0 + blockIdx.x;
   const int tid = threadIdx.x;
   const PointConst P = pc[k];
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   __shared__ double tco[CHEB_N * CHEB_N];   // tco[j][k] = coefficient of t^k in T_j
   __shared__ double cosm[CHEB_N * CHEB_N];  // cosm[j][i] = cos(π j (i + ½) / N), the DCT-II matrix
   for (int e = tid; e < CHEB_N * CHEB_N; e += 256) {
-    tco[e] = kTco.v[e];
+    tco[e] = SUB == 1 ? kTco1.v[e] : kTco2.v[e];
     cosm[e] = cospi((e / CHEB_N) * ((e % CHEB_N) + 0.5) / CHEB_N);
   }
   // This point's s = 8κ·|Q h|² lies in [8κ·d²min/φ²max, 8κ·d²max/φ²min] (the singular
@@ -277,9 +283,12 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   }
 }
 
-cudaError_t launch_table(PointConst* pc, int k0, int kw, double* table, const double* dstat,
+cudaError_t launch_table(int sub, PointConst* pc, int k0, int kw, double* table, const double* dstat,
                          cudaStream_t st) {
-  table_kernel<<<kw, 256, 0, st>>>(pc, k0, table, dstat);
+  if (sub == 2)
+    table_kernel<2><<<kw, 256, 0, st>>>(pc, k0, table, dstat);
+  else
+    table_kernel<1><<<kw, 256, 0, st>>>(pc, k0, table, dstat);
   return cudaGetLastError();
 }
 
@@ -302,11 +311,13 @@ constexpr int BUILD_NE = LIK_BUILD_NE;  // elements per thread evaluated interle
 #ifndef LIK_BUILD_MINB
 #define LIK_BUILD_MINB 4  // 64 registers, 4 blocks (32 warps) per SM: 36.8 vs 40.6 ms per 2,960 C4 points
 #endif
+template <int SUB>
 __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double* __restrict__ coords, SlotGeom g,
                                                     const PointConst* __restrict__ pc, int k0,
                                                     const double* __restrict__ table,
                                                     const double* __restrict__ Bt,
                                                     double* __restrict__ ws) {
+  constexpr int CHEB_SUB = SUB, CHEB_STRIDE = Cheb<SUB>::STRIDE, TABLE_D = Cheb<SUB>::TABLE_D;
   const int slot = blockIdx.y;
   const PointConst P = pc[k0 + slot];
   if (P.mode == MODE_BAD) return;
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
           hx[e] = sx[0][r0 + 4 * (q + e)] - xj;
           hy[e] = sy[0][r0 + 4 * (q + e)] - yj;
         }
-        matern_rho_tableN<BUILD_NE>(P, coef, etab, hx, hy, v, slow, q);
+        matern_rho_tableN<BUILD_NE, SUB>(P, coef, etab, hx, hy, v, slow, q);
 #pragma unroll
         for (int e = 0; e < BUILD_NE; ++e) T[sw_off(r0 + 4 * (q + e), c)] = v[e];
       }
@@ -400,11 +411,14 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
   }
 }
 
-cudaError_t launch_build(const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
+cudaError_t launch_build(int sub, const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
                          int kw, const double* table, const double* Bt, double* ws,
                          cudaStream_t st) {
   dim3 grid((g.ntri + g.nt + BUILD_TILES - 1) / BUILD_TILES, kw);
-  build_kernel<<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
+  if (sub == 2)
+    build_kernel<2><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
+  else
+    build_kernel<1><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
   return cudaGetLastError();
 }
 
