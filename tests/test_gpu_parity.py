@@ -91,7 +91,9 @@ def test_parity_full_config(ctx, orc, name):
 
 
 @pytest.mark.parametrize("n,p,M", [(5, 1, 1), (8, 3, 2), (63, 2, 3), (64, 2, 4), (65, 3, 3),
-                                   (127, 4, 5), (129, 1, 7), (191, 5, 11), (250, 2, 30)])
+                                   (127, 4, 5), (129, 1, 7), (191, 5, 11), (250, 2, 30),
+                                   # both Matérn table layouts at their switch (n = 256)
+                                   (255, 3, 5), (256, 2, 4), (300, 4, 7)])
 def test_parity_ragged_sizes(ctx, orc, n, p, M):
     rng = np.random.default_rng(1000 + n)
     side = 9000.0 * math.sqrt(n / 224.0)
