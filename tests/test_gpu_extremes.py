@@ -38,9 +38,15 @@ def ctx():
     c.close()
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
+# C1 / C2 take the whole-octave table (n < 256), n300 the half-octave one (as C3-C5)
+@pytest.mark.parametrize("name", ["C1", "C2", "n300"])
 def test_matern_build_extremes(ctx, orc, name):
-    coords, y, X = synthgen.make_dataset(name)
+    if name == "n300":
+        base = synthgen.CONFIGS["C3"]
+        coords, y, X = synthgen.make_dataset(
+            synthgen.Config("n300", 300, base.p, 1, base.M, base.iso, base.layout, "n300"), seed=11)
+    else:
+        coords, y, X = synthgen.make_dataset(name)
     d = np.sqrt(((coords[:, None, :] - coords[None, :, :]) ** 2).sum(-1))
     spacing = float(np.median(np.sort(d, axis=1)[:, 1]))
     P = _extreme_params(spacing)

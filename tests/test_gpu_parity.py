@@ -57,9 +57,18 @@ def _oracle(orc, coords, y, X, P, lam):
 
 
 # --------------------------------------------------------------------------- matern_build
-@pytest.mark.parametrize("name", ["C1", "C2"])
+def _inputs_n(n, K, seed=11):
+    """C3-shaped inputs with an arbitrary number of sites."""
+    base = synthgen.CONFIGS["C3"]
+    cfg = synthgen.Config(f"n{n}", n, base.p, K, base.M, base.iso, base.layout, f"n{n}")
+    coords, y, X = synthgen.make_dataset(cfg, seed=seed)
+    return coords, y, X, synthgen.make_params(cfg, K, seed=seed + 1), synthgen.make_lambdas(cfg.M)
+
+
+# C1 / C2 take the whole-octave table (n < 256), n300 the half-octave one (as C3-C5)
+@pytest.mark.parametrize("name", ["C1", "C2", "n300"])
 def test_matern_build_elementwise(ctx, orc, name):
-    coords, y, X, P, lam = synthgen.make_inputs(name, K=64)
+    coords, y, X, P, lam = _inputs_n(300, 64) if name == "n300" else synthgen.make_inputs(name, K=64)
     P = P[:12].copy()
     P[0, 1] = 100.0     # κ-fixed extremes
     P[1, 1] = 0.5
