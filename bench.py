@@ -1,21 +1,31 @@
 """Benchmark of the hot path: profile-likelihood parameter points per second at
 n = 2000 (BASELINE.json configs[3], "C4"), FP64.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C5|...]
+                    [--scaling strong|weak] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
 
-A "step" is one lik_eval_batch_device call over the whole per-rank batch of
-K_pts = 20,000 parameter points × 5 Box-Cox λ (all of SURVEY §8(a): prep,
-matern_build, Cholesky, solve, cross products, epilogue), inputs resident in
-HBM.  Multi-GPU is weak scaling: every rank evaluates its own 20,000 points
-(points sharded k ≡ rank mod N from one N·20,000-point set) and the result
-tables are all-gathered over NCCL (the one exchange step).  `value` = all
-points processed ÷ max-over-ranks device time.  The L2 (126 MB) is flushed
-with a 256 MiB write before every timed step.
+A "step" is one lik_eval_batch_device call over the rank's share of the batch
+(all of SURVEY §8(a): prep, matern_build, Cholesky, solve, cross products,
+epilogue), inputs resident in HBM, plus the one exchange step at N > 1: an
+all-gather of the result tables over NCCL.  C4 = 20,000 parameter points × 5
+Box-Cox λ; C5 (the 8-GPU large-matrix stress config) = 4,000 points × 10 λ at
+n = 5,000.  Multi-GPU defaults to STRONG scaling, as BASELINE.json states the
+configs ("20,000 points sharded across 1/2/4/8 B200"): the config's K points are
+sharded k ≡ rank (mod N) (strided, balancing the κ-dependent cost);
+`--scaling weak` gives every rank its own K points instead.  `value` = all points
+processed ÷ the max-over-ranks device time.  The L2 (126 MB) is flushed with a
+256 MiB write before every timed step.
 
-`e2e` is the same metric through the host-pointer ABI call lik_eval_batch:
-host→device copy of the step's inputs from pinned memory, the path, and the
-device→host copy of the outputs, all inside the timed region.
+With `--gpus N > 1` and no torchrun environment (WORLD_SIZE unset), bench.py
+starts the N ranks itself through torch.distributed.run (127.0.0.1) and passes
+rank 0's line through; under torchrun, --gpus must equal WORLD_SIZE.  NCCL's
+communicator-init lines (NCCL_DEBUG=INFO, subsystem INIT, unless set) go to
+stderr, stdout carries only the JSON line.
+
+`e2e` is the same metric through the host-pointer API: lik_eval_batch at N = 1
+(host→device copy of the step's inputs, the path, device→host copy of the
+outputs, all inside the timed region) and multi.eval_sharded at N > 1.
 
 `--impl reference` times the CPU oracle (oracle/, the parity reference) on the
 host cores over a bounded sample of the same workload.
@@ -38,7 +48,7 @@ sys.path.insert(0, ROOT)
 
 import synthgen  # noqa: E402
 
-WORKLOAD = "C4"
+WORKLOAD = "C4"  # default workload (--config)
 METRIC = "profile-likelihood param points/sec at n=2000 (1/2/4/8 B200); FP64 TFLOP/s vs peak"
 UNIT = "points/s"
 PHASE0 = os.path.join(ROOT, "profiles", "r01", "phase0_fp64_peaks.jsonl")
@@ -132,7 +142,7 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(coords, y, X, P, lam, budget_s=20.0):
+def cpu_baseline(cfg, coords, y, X, P, lam, budget_s=20.0):
     """The oracle, as it stands, on the host cores over a bounded sample of points."""
     import oracle
     T = os.cpu_count() or 1
@@ -148,24 +158,24 @@ def cpu_baseline(coords, y, X, P, lam, budget_s=20.0):
         oracle.eval_batch(coords, y, X, P[T:T * rounds], lam, nthreads=T)
         tt += time.perf_counter() - t0
         npts += T * (rounds - 1)
-    K_full = synthgen.CONFIGS[WORKLOAD].K
     return {"value": npts / tt, "unit": UNIT, "cores": T, "kind": "oracle", "cpu_model": cpu_model(),
-            "sample": f"{npts} points of {WORKLOAD} (n=2000, p=5, M=5) over {T} threads, {tt:.1f} s",
-            "extrapolated_full_config_hours": K_full / (npts / tt) / 3600.0}
+            "sample": f"{npts} points of {cfg.name} (n={cfg.n}, p={cfg.p}, M={cfg.M}) over {T} threads, {tt:.1f} s",
+            "extrapolated_full_config_hours": cfg.K / (npts / tt) / 3600.0}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle timed on the box's host cores."""
+    """--impl reference: the CPU oracle timed on the box's host cores (rank 0 only;
+    the other ranks exit without work)."""
     if rank != 0:
         return
     import oracle
     oracle.build()
-    cfg = synthgen.CONFIGS[WORKLOAD]
+    cfg = synthgen.CONFIGS[args.config]
     coords, y, X = synthgen.make_dataset(cfg)
     P = synthgen.make_params(cfg)
     lam = synthgen.make_lambdas(cfg.M)
     T = os.cpu_count() or 1
-    pts_per_step = T  # one C4 point per host thread per step (~3 s of CPU each)
+    pts_per_step = T  # one point per host thread per step (C4: ~3 s of CPU each)
     for w in range(args.warmup):
         oracle.eval_batch(coords, y, X, P[w * T:(w + 1) * T][:1], lam, nthreads=1)
     times = []
@@ -178,11 +188,11 @@ def run_reference(args, rank, world):
     value = pts_per_step / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{WORKLOAD}: {cfg.desc}", "n": cfg.n, "p": cfg.p, "M": cfg.M,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": cfg.n, "p": cfg.p, "M": cfg.M,
                        "K_per_step": pts_per_step, "parallelism": "host threads"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle",
-                             "sample": f"{pts_per_step} points of {WORKLOAD} per step, {T} threads"},
+                             "sample": f"{pts_per_step} points of {cfg.name} per step, {T} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -198,26 +208,75 @@ def _reserve_stdout():
     return out
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start the N ranks through
+    torch.distributed.run on 127.0.0.1; rank 0's JSON line reaches our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
+def probe_ranks(args, rank, world):
+    """--probe-ranks: the launch check used by the CPU tests — every rank joins a gloo
+    group and rank 0 prints who came (no GPU work)."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank, int(os.environ.get("LOCAL_RANK", "0"))], dtype=torch.int64)
+    got = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(got, t)
+    if rank == 0:
+        print(json.dumps({"probe": True, "world": world, "gpus": args.gpus, "backend": dist.get_backend(),
+                          "ranks": [int(g[0]) for g in got], "local_ranks": [int(g[1]) for g in got]}),
+              flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--points", type=int, default=None, help="points per rank (default 20000)")
+    ap.add_argument("--config", default=WORKLOAD, choices=sorted(synthgen.CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's K points sharded over the ranks (default); "
+                         "weak: K points per rank")
+    ap.add_argument("--points", type=int, default=None,
+                    help="points (strong: in total, weak: per rank; default: the config's K)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="use torch.distributed (NCCL) even with one process: runs the multi-GPU "
                          "code path (checksum, all-gather, max over ranks) on a single GPU")
+    ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and args.gpus != world:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.probe_ranks:
+        probe_ranks(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
 
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator-init lines on stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     json_out = _reserve_stdout()
     import torch
     import torch.distributed as dist
@@ -231,16 +290,19 @@ def main():
     if use_dist:
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29571")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
 
-    cfg = synthgen.CONFIGS[WORKLOAD]
-    K = args.points or cfg.K
+    cfg = synthgen.CONFIGS[args.config]
+    strong = args.scaling == "strong"
+    K_total = (args.points or cfg.K) * (1 if strong else world)
     coords, y, X = synthgen.make_dataset(cfg)
-    Pall = synthgen.make_params(cfg, K * world)
+    Pall = synthgen.make_params(cfg, K_total)
     P = np.ascontiguousarray(Pall[rank::world])  # strided sharding balances κ-dependent cost
+    K = P.shape[0]
+    K_max = multi.local_count(K_total, 0, world)  # the largest shard (rank 0)
     lam = synthgen.make_lambdas(cfg.M)
     n, p, M = cfg.n, cfg.p, cfg.M
     r = M + p
@@ -253,13 +315,14 @@ def main():
     out = lik.Ctx.alloc_outputs(K, M, p, dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     pack_w = multi.pack_width(M, p)
-    gathered = torch.empty((world * K, pack_w), dtype=torch.float64, device=dev) if use_dist else None
+    gathered = torch.empty((world * K_max, pack_w), dtype=torch.float64, device=dev) if use_dist else None
 
     def step():
-        ctx.eval_batch_device(dc, dy, dX, dp, dl, out=out, stream=st)
+        if K:
+            ctx.eval_batch_device(dc, dy, dX, dp, dl, out=out, stream=st)
         if use_dist:  # the one exchange step: all-gather of the result tables (NCCL / NVLink)
             with torch.cuda.stream(st):
-                dist.all_gather_into_tensor(gathered, multi.pack(out, M, p, K))
+                dist.all_gather_into_tensor(gathered, multi.pack(out, M, p, K_max))
 
     for _ in range(args.warmup):
         with torch.cuda.stream(st):
@@ -292,22 +355,21 @@ def main():
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    total_pts = K * world
-    value = total_pts / (ms / 1e3)
+    value = K_total / (ms / 1e3)
     F = dense_flops_per_point(n, r)
-    ok_frac = float((out["status"] == 0).float().mean().item())
+    ok_frac = float((out["status"] == 0).float().mean().item()) if K else 1.0
 
-    # ---- e2e through the host-pointer ABI (pinned host inputs, copies inside the timed region)
+    # ---- e2e through the host-pointer API (pinned host inputs, copies inside the timed region)
     hin = [torch.tensor(a).pin_memory() for a in (coords, y, X, P, lam)]
     hn = [h.numpy() for h in hin]
     e2e_ctx = lik.create(local)
-    e2e_ctx.eval_batch(*hn)  # warm (allocations)
     torch.cuda.synchronize()
     if use_dist:
         dist.barrier()
     e2e_steps = max(1, min(args.steps, 2))
     if not use_dist:
         # lik_eval_batch: host inputs in, host outputs back (one C-ABI call)
+        e2e_ctx.eval_batch(*hn)  # warm (allocations)
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             res = e2e_ctx.eval_batch(*hn)
@@ -325,11 +387,11 @@ def main():
             res = multi.eval_sharded(e2e_ctx, coords, y, X, Pall, lam, dev)
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         h2d = sum(a.nbytes for a in hn)  # coords, y, X, this rank's params, λ
-        d2h = world * multi.local_count(K * world, 0, world) * pack_w * 8
+        d2h = world * K_max * pack_w * 8
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if use_dist:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = total_pts / float(te.item())
+    e2e_value = K_total / float(te.item())
     e2e_ctx.close()
 
     if rank == 0:
@@ -340,19 +402,23 @@ def main():
         traffic, traffic_note = None, None
         try:
             tj = json.load(open(TRAFFIC))
-            pts_per_launch = args.steps * K / chol_n if chol_n else K
-            traffic = tj["dram_bytes_per_point"] * pts_per_launch
-            traffic_note = (f"dram_bytes_read+write per point from one ncu --set full capture "
-                            f"({tj['points_per_launch']}-point launch, {tj['source']}) x "
-                            f"{pts_per_launch:.0f} points per launch here")
+            if tj.get("n", 2000) == n:
+                pts_per_launch = args.steps * K / chol_n if chol_n else K
+                traffic = tj["dram_bytes_per_point"] * pts_per_launch
+                traffic_note = (f"dram_bytes_read+write per point from one ncu --set full capture "
+                                f"({tj['points_per_launch']}-point launch, {tj['source']}) x "
+                                f"{pts_per_launch:.0f} points per launch here")
         except Exception:
             pass
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{WORKLOAD}: {cfg.desc}", "n": n, "p": p, "M": M,
-                       "K_per_rank": K, "parallelism": f"points sharded over {world} GPU(s)",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n, "p": p, "M": M,
+                       "K_total": K_total, "K_rank0": K,
+                       "parallelism": f"points sharded k = rank mod {world} over {world} GPU(s), "
+                                      f"one NCCL all-gather of the result tables" if use_dist else
+                                      "1 GPU",
                        "l2": "flushed (256 MiB write) before every timed step",
                        "wall_s_timed_region": round(t_wall, 3)},
             "fp64_tflops": value * F / 1e12,
@@ -363,7 +429,7 @@ def main():
                          "traffic_note": traffic_note,
                          "peak_source": peak_src,
                          "algorithmic": "n^3/3 + n^2 r + n r^2 FP64 flops per point (SURVEY §8(d)), "
-                                        "x points per launch / launch duration (CUDA events on the launching stream)",
+                                        "x points per launch / launch duration (CUDA events on the launching stream), rank 0",
                          "share_of_step": chol_ms / (args.steps * ms_local) if ms_local else None},
             "matern_build": {  # table + build per step: ρ evaluations and workspace bytes written
                 "evals_per_s": K * n * (n - 1) / 2 / (build_ms / args.steps / 1e3) if build_ms > 0 else None,
@@ -379,7 +445,7 @@ def main():
             "input_hash": synthgen.input_hash(coords, y, X, P, lam),
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(coords, y, X, P, lam)
+            line["cpu_baseline"] = cpu_baseline(cfg, coords, y, X, P, lam)
         print(json.dumps(line), file=json_out, flush=True)
     ctx.close()
     if use_dist:

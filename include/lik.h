@@ -38,6 +38,10 @@
  *   - Results are bitwise deterministic for given inputs, independent of K,
  *     the wave size, the stream and the number of GPUs.
  *   - One lik_ctx per host thread; a ctx is bound to one CUDA device.
+ *   - The device work of successive calls on one ctx runs in call order even when
+ *     they are enqueued on different streams (each call's work waits on an event
+ *     the previous call recorded at its end), because they share the ctx's
+ *     workspace.  Caller buffers follow the usual stream rules.
  * ========================================================================== */
 #ifndef LIK_H_
 #define LIK_H_
@@ -65,7 +69,9 @@ enum {
   LIK_PT_OK = 0,
   LIK_PT_V_NOT_PD = 1,    /* a Cholesky pivot of V <= n·eps·max V_ii (R11) */
   LIK_PT_XVX_NOT_PD = 2,  /* a pivot of XᵀV⁻¹X <= p·eps·max diag (Step 5) */
-  LIK_PT_NEG_RESID = 3,   /* ssqResidual = ssqYX − ssqBetahat < −1e-8·ssqYX (Step 8, R12) */
+  LIK_PT_NEG_RESID = 3,   /* for some λ_m, Step 8's ssqResidual = y'ᵀV⁻¹y' − ssqBetahat is not
+                             > 1e-10·y'ᵀV⁻¹y' (R12): y'_m numerically in
+                             span(X), or negative by rounding.  Only those λ columns fail. */
   LIK_PT_BAD_PARAM = 4    /* φX <= 0, κ <= 0, ν² < 0, φR <= 0 or a non-finite parameter */
 };
 
@@ -141,7 +147,8 @@ int lik_eval_batch_device_ex(lik_ctx* ctx, int n, int p, const double* coords, c
  * All pointers are device pointers; the call is enqueued on `cuda_stream`.
  *   y          n      the response (Jacobian term Σ log y)
  *   ssqYX      K×r×r  Table-1 cross products, r = M + p;  logdetV K;  status K
- *              (points with status != 0 are skipped);  lambdas M
+ *              (points with status other than OK / NEG_RESID are skipped; a
+ *              NEG_RESID point only in its failed λ columns, R12);  lambdas M
  *   beta_grid  p×G    values b of each coefficient β_a;  prof_beta p×G:
  *              ℓ_p(β_a = b) = max over (k, m) of ℓ with β_{−a}, σ² profiled out
  *              (Eq. profilebetai)
@@ -182,13 +189,14 @@ void lik_dataset_destroy(lik_dataset* ds);
 /* Points per wave, i.e. per build/factor launch (0 = automatic: the fewest
  * waves of at most 16 × (2 × #SMs) points within half the free HBM, each a
  * multiple of 2 × #SMs except the last;
- * an explicit value is capped at 85 % of free HBM).  The workspace holds one
+ * an explicit value is capped at 85 % of free HBM and at 65,535; if the
+ * allocation fails, the wave is re-sized from a fresh free-memory query).  The workspace holds one
  * slot per wave point (C4: 17.9 MB).  Results do not depend on it
  * (determinism tests). */
 int lik_set_wave_points(lik_ctx* ctx, int points_per_wave);
 
 /* Debug / parity entry: the dense V = R + ν²I (n×n full, row-major) for each
- * of K points, written by the same matern_build kernel the hot path uses.
+ * of K ≤ 65,535 points, written by the same matern_build kernel the hot path uses.
  * Device pointers; synchronous.  Same validation as lik_eval_batch_device
  * for n, coords and params (bad points give an all-NaN matrix). */
 int lik_debug_build_V(lik_ctx* ctx, int n, const double* coords, int K, const double* params,

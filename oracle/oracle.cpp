@@ -247,7 +247,12 @@ PointResult eval_point(int n, int p, const double* coords, const double* X, int 
   std::vector<double> XX((size_t)p * p), Pd(p);
   for (int a = 0; a < p; ++a)
     for (int b = 0; b < p; ++b) XX[(size_t)a * p + b] = R.ssqYX[(size_t)(M + a) * r + (M + b)];
-  if (ldl(p, XX.data(), Pd.data())) { R.status = PT_XVX_NOT_PD; return R; }
+  if (ldl(p, XX.data(), Pd.data())) {  // failed point: every output NaN / −∞ (ABI convention)
+    R.status = PT_XVX_NOT_PD;
+    R.logdetV = NAN;
+    R.ssqYX.assign((size_t)r * r, NAN);
+    return R;
+  }
   double detReml = 0.0;
   for (int a = 0; a < p; ++a) detReml += std::log(Pd[a]);
   R.detReml = detReml;
@@ -263,6 +268,13 @@ PointResult eval_point(int n, int p, const double* coords, const double* X, int 
     R.ssqBetahat[m] = sb;
     // Step 8: ssqResidual = y'ᵀV⁻¹y' − ssqBetahat
     R.ssqResidual[m] = R.ssqYX[(size_t)m * r + m] - sb;
+    // R12: Step 8's subtraction resolves q only when q > 1e-10·y'ᵀV⁻¹y'; otherwise
+    // (y'_m numerically in span(X), or negative by rounding) the λ column fails:
+    // status NEG_RESID, ℓ_p = −∞, σ̂²/β̂ NaN for that column (the others stand).
+    if (!(R.ssqResidual[m] > 1e-10 * R.ssqYX[(size_t)m * r + m])) {
+      R.status = PT_NEG_RESID;
+      continue;
+    }
     // β̂ = (XᵀV⁻¹X)⁻¹ XᵀV⁻¹y' (Eq. betahat) = Q⁻ᵀ P⁻¹ c (back substitution)
     for (int a = p - 1; a >= 0; --a) {
       double s = c[a] / Pd[a];
@@ -435,7 +447,8 @@ void oracle_profiles(int n, int p, int K, int M, const double* ssqYX, const doub
   for (int e = 0; e < Sg; ++e) out_sigma[e] = -INFINITY;
   for (int m = 0; m < M; ++m) out_lambda[m] = -INFINITY;
   for (int k = 0; k < K; ++k) {
-    if (status[k] != 0) continue;
+    // failed points are skipped; a NEG_RESID point only in its failed λ columns (R12)
+    if (status[k] != PT_OK && status[k] != PT_NEG_RESID) continue;
     const double* C = ssqYX + (size_t)k * r * r;
     auto c = [&](int i, int j) { return C[(size_t)i * r + j]; };
     // full XᵀV⁻¹X factor for β̂ (σ and λ profiles)
@@ -452,6 +465,7 @@ void oracle_profiles(int n, int p, int K, int M, const double* ssqYX, const doub
       double sb = 0.0;
       for (int a = 0; a < p; ++a) sb += u[a] * u[a] / Dx[a];
       const double q = c(m, m) - sb;
+      if (!(q > 1e-10 * c(m, m))) continue;  // R12: the column failed
       const double lp = -0.5 * (n * std::log(q / n) + logdetV[k] + n * ln2pi + n) + jac;
       out_lambda[m] = std::max(out_lambda[m], lp);
       for (int t = 0; t < Sg; ++t) {

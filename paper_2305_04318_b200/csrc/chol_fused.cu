@@ -1081,9 +1081,11 @@ __global__ void LIK_CHOL_BOUNDS chol_fused_kernel(CholArgs A) {
       sb += cv[a] * cv[a];  // Step 7: ssqBetahat = cᵀc
     }
     const double yy = Cm[m * 64 + m];
-    double q = yy - sb;  // Step 8: ssqResidual
-    const bool neg = q < -1e-8 * yy;
-    if (!neg && q < 0.0) q = 0.0;  // R12
+    const double q = yy - sb;  // Step 8: ssqResidual
+    // R12: the subtraction resolves q only when q > 1e-10·yy; otherwise the λ
+    // column fails (ℓ_p = −∞, σ̂²/β̂ NaN, status NEG_RESID) — no OK column can
+    // report q ≤ 0 (log σ̂² = −∞ would make ℓ_p = +∞)
+    const bool neg = !(q > 1e-10 * yy);
     for (int a = p - 1; a >= 0; --a) {  // β̂ = Q⁻ᵀ c (Eq. betahat)
       double s = cv[a];
       for (int b = a + 1; b < p; ++b) s -= Q[b * 64 + a] * bt[b];

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/lik.h"
 #include "lik_internal.cuh"
 
@@ -54,6 +56,11 @@ struct lik_ctx {
   double stage_ms[LIK_NSTAGES] = {0, 0, 0, 0};
   long long stage_n[LIK_NSTAGES] = {0, 0, 0, 0};
   std::vector<cudaEvent_t> ev;
+  // Calls may be enqueued on different streams but share the workspace above: each
+  // call's work waits for the previous call's (done_ev, recorded on its stream at
+  // its end), so a later call never overwrites buffers an earlier one still reads.
+  cudaEvent_t done_ev = nullptr;
+  bool done_recorded = false;
 };
 
 // A validated, device-resident dataset (lik_dataset_create): the per-call prep
@@ -199,6 +206,26 @@ struct HostTrace {
   }
 };
 
+// Order this call's work on `st` after the previous call's (any stream).
+cudaError_t after_previous(lik_ctx* c, cudaStream_t st) {
+  return c->done_recorded ? cudaStreamWaitEvent(st, c->done_ev, 0) : cudaSuccess;
+}
+cudaError_t mark_done(lik_ctx* c, cudaStream_t st) {
+  const cudaError_t e = cudaEventRecord(c->done_ev, st);
+  c->done_recorded = e == cudaSuccess;
+  return e;
+}
+
+// NVTX range (header-only nvtx3; a no-op unless a tool such as nsys / ncu --nvtx
+// injects itself).  Host ranges around the enqueue of each stage: under a tool the
+// per-stage kernels are attributed to lik.prep / lik.setup / lik.build / lik.chol.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+
 cudaEvent_t ev_get(lik_ctx* c, size_t i) {
   while (c->ev.size() <= i) {
     cudaEvent_t e;
@@ -227,6 +254,8 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
                double* betahat, double* sigma2hat, double* logdetV, int* status, cudaStream_t st,
                const double* hcoords, const Extras& ex = Extras(), const Prepared* pre = nullptr) {
   HostTrace tr;
+  Nvtx nv_call("lik.eval");
+  CUDA_TRY(c, after_previous(c, st));
   const SlotGeom g = lik::make_geom(n, M + p);
   const size_t slot_bytes = g.slot_d * sizeof(double);
   // Wave size W (points per table/build/chol launch).  All CTAs of a chol launch
@@ -234,42 +263,52 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   // launches lose less to that tail (the CTA scheduler backfills within a launch):
   // by default the fewest waves of at most 16 × (resident CTAs per GPU) points that
   // fit in half the free HBM, each a whole number of CTA rounds except the last.
-  // lik_set_wave_points overrides (85 % cap).
-  int W;
-  {
-    size_t avail;
-    if (c->avail_K == K && c->avail_slot == slot_bytes) {
-      avail = c->avail_cache;
-    } else {
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      avail = fr + c->ws_bytes;
-      c->avail_cache = avail;
-      c->avail_slot = slot_bytes;
-      c->avail_K = K;
-    }
-    const size_t cap = (size_t)(0.85 * (double)avail) / slot_bytes;
-    if (cap < 1) return fail(c, LIK_ENOMEM, "one workspace slot (%zu bytes) exceeds free HBM", slot_bytes);
-    if (c->wave_points > 0) {
-      W = (int)std::min<size_t>((size_t)std::min(c->wave_points, K), cap);
-    } else {
-      // waves are whole multiples of the resident CTAs (res), so only the last
-      // launch ends on a partly filled round
-      const int res = c->nsm * lik::chol_ctas_per_sm();
-      const size_t half = std::max<size_t>(1, (size_t)(0.5 * (double)avail) / slot_bytes);
-      int wmax = (int)std::min<size_t>((size_t)16 * res, half);
-      if (wmax >= res) wmax -= wmax % res;
-      const int nw = (K + wmax - 1) / wmax;
-      W = (K + nw - 1) / nw;
-      if (W > res) W = std::min({wmax, (W + res - 1) / res * res, K});
-    }
-  }
+  // lik_set_wave_points overrides (85 % cap).  The build grid carries the wave in
+  // gridDim.y, so W ≤ 65,535.
+  auto wave_size = [&](size_t avail) -> int {
+    const size_t cap = std::min<size_t>((size_t)(0.85 * (double)avail) / slot_bytes, 65535);
+    if (cap < 1) return 0;
+    if (c->wave_points > 0) return (int)std::min<size_t>((size_t)std::min(c->wave_points, K), cap);
+    // waves are whole multiples of the resident CTAs (res), so only the last
+    // launch ends on a partly filled round
+    const int res = c->nsm * lik::chol_ctas_per_sm();
+    const size_t half = std::max<size_t>(1, (size_t)(0.5 * (double)avail) / slot_bytes);
+    int wmax = (int)std::min<size_t>(std::min<size_t>((size_t)16 * res, half), 65535);
+    if (wmax >= res) wmax -= wmax % res;
+    const int nw = (K + wmax - 1) / wmax;
+    int w = (K + nw - 1) / nw;
+    if (w > res) w = std::min({wmax, (w + res - 1) / res * res, K});
+    return w;
+  };
+  auto query_avail = [&]() {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t avail = fr + c->ws_bytes;
+    c->avail_cache = avail;
+    c->avail_slot = slot_bytes;
+    c->avail_K = K;
+    return avail;
+  };
+  const bool cached = c->avail_K == K && c->avail_slot == slot_bytes;
+  int W = wave_size(cached ? c->avail_cache : query_avail());
   tr.mark("memgetinfo");
   int rc;
-  if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes))) {
-    c->avail_K = -1;  // query the free memory again next time
-    return rc;
+  // the free-memory figure may be stale (another allocation since it was cached, or
+  // another process): on failure query again and retry with a smaller wave
+  for (int attempt = 0;; ++attempt) {
+    if (W < 1) {
+      c->avail_K = -1;
+      return fail(c, LIK_ENOMEM, "one workspace slot (%zu bytes) exceeds free HBM", slot_bytes);
+    }
+    if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes)) == LIK_OK) break;
+    cudaGetLastError();  // clear the allocation error
+    if (attempt >= 8) {
+      c->avail_K = -1;
+      return rc;
+    }
+    W = std::min(wave_size(query_avail()), W / 2);
   }
+  c->err.clear();
   size_t pcb = c->pc_cap * sizeof(PointConst);
   if ((rc = ensure(c, &c->pc, &pcb, (size_t)K * sizeof(PointConst)))) return rc;
   c->pc_cap = pcb / sizeof(PointConst);
@@ -300,6 +339,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     }
     tr.mark("morton+h2d");
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
+    Nvtx nv("lik.prep");
     CUDA_TRY(c, lik::launch_prep(coords, y, X, lambdas, dperm, n, p, M, g.nt * lik::TB, c->coords_p,
                                  c->bt, c->S, st));
     CUDA_TRY(c, lik::launch_dist_range(c->coords_p, n, c->S + 1, st));
@@ -308,12 +348,18 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     S = c->S;
   }
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
-  CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
+  {
+    Nvtx nv("lik.setup");
+    CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
+  }
   if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   for (int w = 0; w < nwaves; ++w) {
     const int k0 = w * W, kw = std::min(W, K - k0);
-    CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, k0, kw, c->table, S + 1, st));
-    CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
+    {
+      Nvtx nvb("lik.build");
+      CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, k0, kw, c->table, S + 1, st));
+      CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
+    }
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
     a.ws = c->ws;
@@ -335,10 +381,12 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     a.ssqResidual = ex.ssqResidual;
     a.loglik_reml = ex.loglik_reml;
     a.sigma2hat_reml = ex.sigma2hat_reml;
+    Nvtx nvc("lik.chol");
     CUDA_TRY(c, lik::launch_chol(a, kw, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   }
   tr.mark("launches");
+  CUDA_TRY(c, mark_done(c, st));
   if (timing) {
     CUDA_TRY(c, cudaEventSynchronize(c->ev[ei - 1]));
     float ms = 0.f;
@@ -385,7 +433,9 @@ int lik_create(lik_ctx** out, int cuda_device, unsigned flags) {
   c->device = cuda_device;
   c->flags = flags;
   c->nsm = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming) != cudaSuccess) {
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return LIK_ECUDA;
   }
@@ -407,6 +457,7 @@ void lik_destroy(lik_ctx* c) {
   cudaFree(c->prof_scratch);
   cudaFree(c->io);
   for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->done_ev) cudaEventDestroy(c->done_ev);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -526,9 +577,12 @@ int lik_profiles_device(lik_ctx* c, int n, int p, int K, int M, const double* y,
   const size_t need = lik::profile_scratch(p, K, M, G, Sg) * sizeof(double);
   int rc;
   if ((rc = ensure(c, &c->prof_scratch, &c->prof_scratch_bytes, need))) return rc;
+  const cudaStream_t st = (cudaStream_t)cuda_stream;
+  CUDA_TRY(c, after_previous(c, st));
   CUDA_TRY(c, lik::launch_profiles(n, p, K, M, y, ssqYX, logdetV, status, lambdas, G, beta_grid,
                                    prof_beta, Sg, sigma_grid, prof_sigma, prof_lambda,
-                                   c->prof_scratch, (cudaStream_t)cuda_stream));
+                                   c->prof_scratch, st));
+  CUDA_TRY(c, mark_done(c, st));
   return LIK_OK;
 }
 
@@ -651,7 +705,8 @@ int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const doub
   if (!c) return LIK_EINVAL;
   c->err.clear();
   if (any_null({coords, params, V})) return fail(c, LIK_EINVAL, "NULL pointer argument");
-  if (n < 1 || K < 1) return fail(c, LIK_EINVAL, "n = %d, K = %d", n, K);
+  if (n < 1 || K < 1 || K > 65535)
+    return fail(c, LIK_EINVAL, "n = %d, K = %d (1 <= K <= 65535 per debug call)", n, K);
   CUDA_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = c->own_stream;
   std::vector<double> hc(2 * (size_t)n);
@@ -668,11 +723,13 @@ int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const doub
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)K * lik::TABLE_D * sizeof(double))))
     return rc;
   if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));
+  CUDA_TRY(c, after_previous(c, st));
   CUDA_TRY(c, lik::launch_dist_range(coords, n, c->S + 1, st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
   CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, 0, K, c->table, c->S + 1, st));
   CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords, g, c->pc, 0, K, c->table, nullptr, c->ws, st));
   CUDA_TRY(c, lik::launch_unpack_V(g, c->pc, K, c->ws, V, st));
+  CUDA_TRY(c, mark_done(c, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
   return LIK_OK;
 }

@@ -81,15 +81,11 @@ inline SlotGeom make_geom(int n, int r) {
 enum { MODE_BESSEL = 0, MODE_GAUSS = 1, MODE_BAD = 2 };
 struct PointConst {
   double cX, sX, sY, cY;   // u/φX = cX hx − sX hy,  v/φY = sY hx + cY hy
-  double kappa, sqrt8k;    // κ, √(8κ)
+  double kappa;            // κ
   double eightk;           // 8κ (s = z² = 8κ d², exact)
-  double mu;               // fractional order μ = κ − nl ∈ [−1/2, 1/2)
-  double lnpref;           // (1−κ) ln 2 − ln Γ(κ)
-  double gam1, gam2;       // Temme constants of μ
-  double gampl, gammi;     // 1/Γ(1+μ), 1/Γ(1−μ)
-  double fact;             // πμ / sin(πμ)
+  double inv4k;            // 1/(4κ)  (the Gamma-mixture quadrature, matern_rho.cuh)
+  double lnC;              // κ ln κ − κ − ln Γ(κ)
   double nugget;           // ν²
-  int nl;                  // forward-recurrence steps (κ = μ + nl)
   int mode;                // MODE_*
   int e_zero;              // ρ ≡ 0 (ln ρ < −750) for s = z² ≥ 2^e_zero (set by table_kernel)
   int olo, ohi;            // table octaves built for this point (its range of s ± 1 octave)

@@ -5,7 +5,7 @@
 //   build_kernel  — a2 "matern_build": V = R + ν²I tiles (P:86, P:311 Step 1)
 #include <algorithm>
 #include <cfloat>
-#include "bessel_k.cuh"
+#include "matern_rho.cuh"
 #include "lik_internal.cuh"
 
 namespace lik {
@@ -90,22 +90,13 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
   P.sY = s / phiY;
   P.cY = c / phiY;
   P.kappa = kappa;
-  P.sqrt8k = sqrt(8.0 * kappa);
   P.eightk = 8.0 * kappa;
+  P.inv4k = 0.25 / kappa;
   P.nugget = nug;
-  int nl = 0;
-  double mu = 0.0;
-  if (P.mode == MODE_BESSEL) {
-    nl = (int)(kappa + 0.5);
-    mu = kappa - nl;
-  }
-  P.nl = nl;
-  P.mu = mu;
   P.e_zero = 1 << 20;  // set by table_kernel
   P.olo = 0;
   P.ohi = CHEB_NOCT - 1;
-  P.lnpref = ok && P.mode == MODE_BESSEL ? (1.0 - kappa) * 0.69314718055994530942 - lgamma(kappa) : 0.0;
-  temme_constants(mu, &P.gam1, &P.gam2, &P.gampl, &P.gammi, &P.fact);
+  P.lnC = ok && P.mode == MODE_BESSEL ? matern_lnC(kappa) : 0.0;
   pc[k] = P;
 }
 
@@ -185,27 +176,42 @@ __device__ const TcoTable<Cheb<1>::N> kTco1 = make_tco<Cheb<1>::N>();
 __device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
 
 // ---------------------------------------------------------------------------
-// table: one block per point of the wave.  ln ρ is evaluated exactly (Temme /
-// CF2 + recurrence) at the interval edges and at CHEB_N Chebyshev nodes of every
-// interval (CHEB_SUB per binary octave of s = z²) below the underflow octave
-// e_zero, detrended by the line through the edge values (so the DCT works on a
-// small function) and turned into Chebyshev coefficients (DCT-II), then monomial
-// ones with the line added back.  ln ρ(√s) is analytic on each interval (its only
-// finite singularity is the branch point s = 0: 3 half-widths from the centre of
-// a whole octave, 5 from that of [1, 1.5)·2^e), so degree 19 resp. 15 reaches the
-// FP64 rounding floor (~1e-16·max(1, |ln ρ|)), DESIGN.md §5.
+// table: one block per point of the wave.  ln ρ is evaluated exactly (the
+// Gamma-mixture quadrature of matern_rho.cuh) at the interval edges and at CHEB_N
+// Chebyshev nodes of every interval (CHEB_SUB per binary octave of s = z²) below
+// the underflow octave e_zero, detrended by the line through the edge values (so
+// the DCT works on a small function) and turned into Chebyshev coefficients
+// (DCT-II), then monomial ones with the line added back.  ln ρ(√s) is analytic on
+// each interval (its only finite singularity is the branch point s = 0: 3
+// half-widths from the centre of a whole octave, 5 from that of [1, 1.5)·2^e), so
+// degree 19 resp. 15 reaches the FP64 rounding floor (~1e-16·max(1, |ln ρ|)),
+// DESIGN.md §5.
+//
+// The nodes of one octave share a quadrature grid: one warp per octave, one lane
+// per Chebyshev node (SUB = 2: 2 × 16 = 32 lanes; SUB = 1: 20).  The grid step is
+// the one of the octave's largest s (the finest: the peak's curvature κr grows with
+// s), and the grid spans the union of the nodes' windows — from where G(·; 2^e)
+// falls 40 below its peak on the left (the smallest s has the longest left tail) to
+// where G(·; 2^{e+1}) does on the right.  Per grid node the warp computes
+// A = κ(x − (e^x − 1)) and B = e^{−x}/(4κ) once (into shared memory), so each lane's
+// G(x; s) = A − s·B costs one FMA and its term one exp.
 // ---------------------------------------------------------------------------
+constexpr int QCAP = 64;  // grid nodes per warp chunk
+
 template <int SUB>
 __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc, int k0,
                                                     double* __restrict__ table,
                                                     const double* __restrict__ dstat) {
   constexpr int CHEB_SUB = SUB, CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
   constexpr int CHEB_NINT = Cheb<SUB>::NINT, TABLE_D = Cheb<SUB>::TABLE_D;
+  static_assert(CHEB_SUB * CHEB_N <= 32, "one lane per node of an octave");
+  static_assert(CHEB_NINT * CHEB_N >= 8 * 2 * QCAP, "quadrature scratch fits in cheb[]");
   const int k = k0 + blockIdx.x;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const PointConst P = pc[k];
   if (P.mode != MODE_BESSEL) return;
   __shared__ double f[CHEB_NINT * CHEB_N];
+  __shared__ double cheb[CHEB_NINT * CHEB_N];  // also the warps' quadrature scratch
   __shared__ double edge[CHEB_NINT + 1];
   __shared__ int ez;
   __shared__ double tco[CHEB_N * CHEB_N];   // tco[j][k] = coefficient of t^k in T_j
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   const int ohi = s_hi > 0.0 ? max(olo, min(CHEB_NOCT - 1, ilogb(s_hi) - CHEB_ELO + 1)) : olo;
   // interval edges: s = 2^(ELO + iv/SUB) · (1 + (iv mod SUB)/SUB)
   for (int iv = olo * CHEB_SUB + tid; iv <= (ohi + 1) * CHEB_SUB; iv += 256)
-    edge[iv] = log_rho_exact(P, sqrt(ldexp(1.0 + (double)(iv % CHEB_SUB) / CHEB_SUB, CHEB_ELO + iv / CHEB_SUB)));
+    edge[iv] = log_rho_exact(P, ldexp(1.0 + (double)(iv % CHEB_SUB) / CHEB_SUB, CHEB_ELO + iv / CHEB_SUB));
   __syncthreads();
   if (tid == 0) {
     int e0 = CHEB_ELO + CHEB_NOCT + 64;  // sentinel: never underflows inside the table range
@@ -240,23 +246,67 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
     pc[k].ohi = ohi;
   }
   __syncthreads();
-  // g = ln ρ(√s) − L_o(x) at the nodes, L_o the line through the octave's edge values
-  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
-    const int iv = idx / CHEB_N, i = idx % CHEB_N;  // interval iv: octave iv/SUB, part iv mod SUB
-    const int e = CHEB_ELO + iv / CHEB_SUB;
-    double v = 0.0;
-    if (e < ez) {
-      const double x = cospi((i + 0.5) / CHEB_N);
-      const double lo = 1.0 + (double)(iv % CHEB_SUB) / CHEB_SUB, hw = 0.5 / CHEB_SUB;
-      const double sn = ldexp(lo + hw * (1.0 + x), e);
-      v = log_rho_exact(P, sqrt(sn)) - 0.5 * (edge[iv] + edge[iv + 1]) - 0.5 * (edge[iv + 1] - edge[iv]) * x;
+  // g = ln ρ(√s) − L_o(x) at the nodes, L_o the line through the interval's edge values
+  {
+    const double kap = P.kappa, i4k = P.inv4k;
+    double* qa = cheb + warp * 2 * QCAP;
+    double* qb = qa + QCAP;
+    const bool active = lane < CHEB_SUB * CHEB_N;
+    const int part = active ? lane / CHEB_N : 0, i = active ? lane % CHEB_N : 0;
+    const double xc = cospi((i + 0.5) / CHEB_N);
+    const double lo = 1.0 + (double)part / CHEB_SUB, hw = 0.5 / CHEB_SUB;
+    for (int o = olo + warp; o <= ohi && CHEB_ELO + o < ez; o += 8) {
+      const int e = CHEB_ELO + o;
+      const double s0 = ldexp(1.0, e), s1 = 2.0 * s0;
+      double x0, x1, h0, h;
+      quad_peak_step(kap, s0, x0, h0);
+      quad_peak_step(kap, s1, x1, h);
+      const double a0 = s0 * i4k, a1 = s1 * i4k;
+      const double g0 = quad_G(kap, a0, x0), g1 = quad_G(kap, a1, x1);
+      // left extent from the peak of s0, right extent from the peak of s1
+      int L = 0, R = 0;
+      for (int base = 0; base < kQuadMaxNodes; base += 32) {
+        const unsigned bad = __ballot_sync(0xffffffffu, quad_G(kap, a0, x0 - (base + lane + 1) * h) - g0 < -kQuadCut);
+        L = base + (bad ? __ffs(bad) - 1 : 32);
+        if (bad) break;
+      }
+      for (int base = 0; base < kQuadMaxNodes; base += 32) {
+        const unsigned bad = __ballot_sync(0xffffffffu, quad_G(kap, a1, x1 + (base + lane + 1) * h) - g1 < -kQuadCut);
+        R = base + (bad ? __ffs(bad) - 1 : 32);
+        if (bad) break;
+      }
+      const double xl = x0 - L * h;
+      const int nq = L + (int)ceil((x1 - x0) / h) + R + 1;
+      // this lane's node s and the peak of G(·; s) (the log-sum reference)
+      const double sn = ldexp(lo + hw * (1.0 + xc), e);
+      double xs, hs;
+      quad_peak_step(kap, sn, xs, hs);
+      const double gs = quad_G(kap, sn * i4k, xs);
+      double sum = 0.0;
+      for (int c0 = 0; c0 < nq; c0 += QCAP) {
+        __syncwarp();
+        for (int j = lane; j < QCAP && c0 + j < nq; j += 32) {
+          const double x = xl + (c0 + j) * h;
+          double ex, em;
+          quad_exp(x, ex, em);
+          qa[j] = kap * (x - em);
+          qb[j] = i4k / ex;
+        }
+        __syncwarp();
+        const int cn = min(QCAP, nq - c0);
+        for (int j = 0; j < cn; ++j) sum += exp(fma(-sn, qb[j], qa[j]) - gs);
+      }
+      __syncwarp();
+      if (active) {
+        const int iv = o * CHEB_SUB + part;
+        const double lr = P.lnC + gs + log(h * sum);
+        f[iv * CHEB_N + i] = lr - 0.5 * (edge[iv] + edge[iv + 1]) - 0.5 * (edge[iv + 1] - edge[iv]) * xc;
+      }
     }
-    f[idx] = v;
   }
   __syncthreads();
   // Chebyshev coefficients of g (DCT-II), then monomial coefficients in t (T_j has
   // integer coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
-  __shared__ double cheb[CHEB_NINT * CHEB_N];
   for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
     const int iv = idx / CHEB_N, jj = idx % CHEB_N;
     double cc = 0.0;

@@ -1,0 +1,208 @@
+// Device FP64 Matérn correlation ρ, evaluated without Bessel functions.
+//
+// ρ(d; κ) = 2^{1−κ}/Γ(κ) · z^κ K_κ(z),  z = √(8κ) d          (Eq. matern; R1)
+//
+// With the integral representation (DLMF 10.32.10)
+//   K_κ(z) = ½ (z/2)^κ ∫_0^∞ exp(−t − z²/(4t)) t^{−κ−1} dt
+// and the substitution t = z²/(4w), the prefactor cancels exactly and
+//   ρ = (1/Γ(κ)) ∫_0^∞ w^{κ−1} e^{−w} e^{−s/(4w)} dw,   s = z² = 8κ d²,
+// i.e. ρ = E[exp(−s/(4W))] for W ~ Gamma(κ, 1) — the Matérn correlation as a scale
+// mixture of Gaussians.  Nothing cancels between large terms (ρ ∈ (0, 1], ρ(0) = 1),
+// nothing overflows for large κ at small z and nothing underflows at large z (the sum is
+// carried in log space), and one formula covers every κ < 1e3 (R7: the Gaussian limit
+// exp(−2d²) above).  The build never forms z: only s = 8κ d² (no square root).
+//
+// Quadrature.  With w = κ e^x,
+//   ln ρ = C(κ) + ln ∫_{−∞}^{∞} e^{G(x; s)} dx,
+//   G(x; s) = κ (x − (e^x − 1)) − (s/(4κ)) e^{−x},
+//   C(κ)    = κ ln κ − κ − ln Γ(κ)
+//           = ½ ln κ − ½ ln 2π − Σ_j B_2j / (2j(2j−1) κ^{2j−1})   (Stirling, used for κ ≥ 10,
+//             so the O(κ ln κ) terms cancel analytically, not in floating point).
+// G is strictly concave (G'' = −κe^x − (s/4κ)e^{−x}) and entire, with double-exponential
+// tails, so the trapezoid rule on the whole line converges geometrically in 1/h: its
+// relative error is the Fourier transform of e^G at 2π/h — |Γ(κ + 2πi/h)/Γ(κ)| at s = 0,
+// ≈ exp(−2π²σ²/h²) around a Gaussian-like peak — which stays below 1e-17 for
+//   h ≤ min(0.165, 0.45 σ),  σ² = −1/G''(x*) = 1/(κ r),  r = √(1 + s/κ²)
+// (checked against mpmath for κ ∈ [0.01, 999]).  The peak: G'(x*) = 0 ⇔ e^{x*} = (1 + r)/2.
+// Nodes are summed outwards from the peak until G falls 40 below G(x*) (e^{−40} = 4e-18).
+// Measured against mpmath besselk (50 digits) over κ ∈ [0.01, 999], z ∈ [1e-8, 700]:
+// |Δ ln ρ| ≤ 2.1e-15 · max(1, |ln ρ|) (R8).
+#pragma once
+#include "lik_internal.cuh"
+
+namespace lik {
+
+constexpr double kHalfLn2Pi = 0.91893853320467274178;  // ½ ln 2π
+constexpr double kQuadHmax = 0.165;                    // trapezoid step cap (s → 0, small κ)
+constexpr double kQuadAlpha = 0.45;                    // step / σ
+constexpr double kQuadCut = 40.0;                      // nodes kept while G ≥ G(x*) − 40
+constexpr int kQuadMaxNodes = 1 << 16;                 // per side (only tiny κ at tiny s approach it)
+
+// C(κ) = κ ln κ − κ − ln Γ(κ)  (once per point).
+__device__ inline double matern_lnC(double k) {
+  if (k >= 10.0) {
+    // ln Γ(κ) = (κ − ½) ln κ − κ + ½ ln 2π + Σ_{j=1..8} B_2j / (2j(2j−1) κ^{2j−1}); the first
+    // omitted term is < 2e-18 at κ = 10
+    const double c[8] = {1.0 / 12.0, -1.0 / 360.0, 1.0 / 1260.0, -1.0 / 1680.0,
+                         1.0 / 1188.0, -691.0 / 360360.0, 1.0 / 156.0, -3617.0 / 122400.0};
+    const double k2 = 1.0 / (k * k);
+    double t = c[7];
+#pragma unroll
+    for (int j = 6; j >= 0; --j) t = fma(t, k2, c[j]);
+    return 0.5 * log(k) - kHalfLn2Pi - t / k;
+  }
+  return k * log(k) - k - lgamma(k);
+}
+
+// Peak x* of G(·; s) and the trapezoid step for that s.
+__device__ __forceinline__ void quad_peak_step(double k, double s, double& xs, double& h) {
+  const double q = s / (k * k);
+  const double r = sqrt(1.0 + q);
+  xs = log1p(q / (2.0 * (1.0 + r)));  // ln((1 + r)/2), r − 1 = q/(1 + r) without cancellation
+  h = fmin(kQuadHmax, kQuadAlpha * rsqrt(k * r));
+}
+
+// e^x and e^x − 1 for a quadrature node: expm1 near 0 (where e^x − 1 cancels); e^x
+// itself elsewhere — never 1 + expm1(x), which loses all digits of e^x for x ≲ −30
+// (the left tails of small κ reach x ≈ −40 at the smallest s).
+__device__ __forceinline__ void quad_exp(double x, double& ex, double& em) {
+  ex = exp(x);
+  em = fabs(x) < 0.5 ? expm1(x) : ex - 1.0;
+}
+
+// G(x; s) with a = s/(4κ).
+__device__ __forceinline__ double quad_G(double k, double a, double x) {
+  double ex, em;
+  quad_exp(x, ex, em);
+  return k * (x - em) - a / ex;
+}
+
+// Exact ln ρ at s = z² > 0 (Bessel mode).  Used for the table's interval edges and for
+// the elements outside the point's table (rare); the table nodes use the octave-shared
+// grid of table_kernel, the same rule.
+static __device__ __noinline__ double log_rho_exact(const PointConst& P, double s) {
+  const double k = P.kappa, a = s * P.inv4k;
+  double xs, h;
+  quad_peak_step(k, s, xs, h);
+  const double gs = quad_G(k, a, xs);
+  double sum = 1.0;  // the node at the peak
+  for (int i = 1; i < kQuadMaxNodes; ++i) {
+    const double g = quad_G(k, a, xs + i * h) - gs;
+    if (g < -kQuadCut) break;
+    sum += exp(g);
+  }
+  for (int i = 1; i < kQuadMaxNodes; ++i) {
+    const double g = quad_G(k, a, xs - i * h) - gs;
+    if (g < -kQuadCut) break;
+    sum += exp(g);
+  }
+  return P.lnC + gs + log(h * sum);
+}
+
+// Scaled anisotropic distance d(h)², P:104-120 (R3: φY = φX/φR).
+__device__ __forceinline__ double aniso_d2(const PointConst& P, double hx, double hy) {
+  const double u = P.cX * hx - P.sX * hy;
+  const double v = P.sY * hx + P.cY * hy;
+  return u * u + v * v;
+}
+
+// ρ for a site pair at offset (hx, hy) by direct (exact) evaluation.
+__device__ __forceinline__ double matern_rho_exact(const PointConst& P, double hx, double hy) {
+  const double d2 = aniso_d2(P, hx, hy);
+  if (d2 == 0.0) return 1.0;
+  if (P.mode == MODE_GAUSS) return exp(-2.0 * d2);
+  const double lr = log_rho_exact(P, P.eightk * d2);
+  return lr < -760.0 ? 0.0 : exp(lr);
+}
+
+// 2^(j/16), j = 0..15, correctly rounded (mpmath).  16 entries = 128 bytes: one
+// entry per bank pair, so a half-warp's data-dependent lookups never conflict (a
+// 32-entry table doubled the exp's shared-memory wavefronts).
+static __constant__ double kExp2Tab[16] = {
+    1.0, 1.0442737824274138, 1.0905077326652577, 1.1387886347566916,
+    1.189207115002721, 1.241857812073484, 1.2968395546510096, 1.3542555469368927,
+    1.4142135623730951, 1.4768261459394993, 1.5422108254079407, 1.6104903319492543,
+    1.681792830507429, 1.7562521603732995, 1.8340080864093424, 1.9152065613971474};
+
+// exp(x) for x ≤ 1 (the table path's ρ = exp(ln ρ), ln ρ ≤ 0; x < −760 is clamped there,
+// where the result underflows to 0 — ln ρ reaches far below −746 inside the last
+// non-zero octave for large κ): k = rint(16x/ln 2), r = x − k ln2/16 (Cody-Waite, the
+// high part of ln2/16 has 32 significant bits so k·hi is exact for |k| < 2^21),
+// e^r − 1 by its degree-7 Taylor polynomial (|r| ≤ ln2/32: truncation < 2e-18),
+// e^x = 2^(k>>4) · T[k & 15] · (1 + q), the power of two applied in two exact halves
+// so subnormal results are rounded once.  etab = kExp2Tab copied to shared memory.
+// ≤ 1 ulp (checked against mpmath over [−746, 1]).
+__device__ __forceinline__ double exp_neg(double x, const double* etab) {
+  const double shift = 6755399441055744.0;  // 1.5·2^52: round-to-nearest integer in the low bits
+  x = fmax(x, -760.0);  // keeps both 2^(m/2) factors normal; the product underflows to 0
+  const double kds = fma(x, 23.083120654223414, shift);
+  const double kd = kds - shift;
+  const int k = __double2loint(kds);
+  double r = fma(kd, -0.04332169877307024, x);
+  r = fma(kd, -1.1926343307941173e-11, r);
+  double q = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+  q = fma(q, r, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q *= r;
+  const double tj = etab[k & 15];
+  const double v = fma(tj, q, tj);
+  const int m = k >> 4;
+  // v ∈ [0.98, 2.04]: for m ≥ −1021 the result is normal and v·2^m is exactly v with
+  // m added to its exponent field (an integer add instead of two FP64 multiplies;
+  // bitwise the same result); below, the two-step scale rounds a subnormal once
+  if (m >= -1021) return __longlong_as_double(__double_as_longlong(v) + ((long long)m << 52));
+  const int m1 = m >> 1, m2 = m - m1;
+  const double s1 = __hiloint2double((m1 + 1023) << 20, 0), s2 = __hiloint2double((m2 + 1023) << 20, 0);
+  return (v * s1) * s2;
+}
+
+// NE table evaluations interleaved (independent Horner chains for ILP).  Elements
+// that need the exact path (s = z² outside the point's table, or 0) set bit
+// `bit + e` of `slow`; their returned value is meaningless.
+template <int NE, int SUB>
+__device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const double* coef,
+                                                  const double* etab, const double (&hx)[NE],
+                                                  const double (&hy)[NE], double (&v)[NE],
+                                                  unsigned& slow, int bit) {
+  constexpr int CHEB_SUB = SUB, CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
+  double sv[NE], t[NE], h[NE];
+  int oc[NE];
+  bool zero[NE], in[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    sv[e] = P.eightk * aniso_d2(P, hx[e], hy[e]);  // s = z² (no square root)
+    const int ex = (int)((__double_as_longlong(sv[e]) >> 52) & 0x7ff) - 1023;
+    const int o = ex - CHEB_ELO;
+    zero[e] = ex >= P.e_zero;
+    in[e] = o >= P.olo && o <= P.ohi;
+    oc[e] = min(max(o, P.olo), P.ohi);
+    const int part = CHEB_SUB == 1 ? 0 : (int)((__double_as_longlong(sv[e]) >> 51) & 1);
+    t[e] = sv[e] * __longlong_as_double((long long)(1023 + CHEB_SUB - (oc[e] + CHEB_ELO)) << 52) -
+           (double)(2 * CHEB_SUB + 1 + 2 * part);
+    oc[e] = oc[e] * CHEB_SUB + part;  // from here on: the interval
+  }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double2 u = reinterpret_cast<const double2*>(coef + oc[e] * CHEB_STRIDE + 2)[CHEB_N / 2 - 1];
+    h[e] = fma(u.y, t[e], u.x);
+  }
+#pragma unroll
+  for (int mm = CHEB_N / 2 - 2; mm >= 0; --mm) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const double2 u = reinterpret_cast<const double2*>(coef + oc[e] * CHEB_STRIDE + 2)[mm];
+      h[e] = fma(fma(h[e], t[e], u.y), t[e], u.x);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double r = exp_neg(coef[oc[e] * CHEB_STRIDE] + h[e], etab);
+    v[e] = zero[e] ? 0.0 : r;
+    slow |= (unsigned)(!zero[e] && !(in[e] && sv[e] > 0.0)) << (bit + e);
+  }
+}
+
+}  // namespace lik

@@ -60,7 +60,9 @@ __global__ void factor_kernel(int p, int K, int M, const double* __restrict__ ss
   double H[PMAX * PMAX], x[PMAX];
   for (int i = 0; i < p; ++i)
     for (int j = 0; j <= i; ++j) H[i * p + j] = C[(size_t)(M + i) * r + (M + j)];
-  const bool ok = status[k] == 0 && chol_small(H, p, p) == 0;
+  // failed points are skipped; a NEG_RESID point only in its failed λ columns (R12,
+  // solve_kernel marks them NaN, which every max below ignores)
+  const bool ok = (status[k] == 0 || status[k] == 3) && chol_small(H, p, p) == 0;
   double* L = Lbuf + (size_t)k * p * p;
   for (int i = 0; i < p; ++i)
     for (int j = 0; j < p; ++j) L[i * p + j] = ok && j <= i ? H[i * p + j] : (ok ? 0.0 : nan);
@@ -98,7 +100,10 @@ __global__ void solve_kernel(int p, int K, int M, const double* __restrict__ ssq
     w[i] = t / L[i * p + i];
     s2 += w[i] * w[i];
   }
-  qfull[e] = C[(size_t)m * r + m] - s2;  // NaN propagates from a failed point's L
+  // Step 8; NaN propagates from a failed point's L; a column whose Step 8 is not
+  // resolved (q ≤ 1e-10·y'ᵀV⁻¹y', R12) is NaN too
+  const double yy = C[(size_t)m * r + m], qv = yy - s2;
+  qfull[e] = qv > 1e-10 * yy ? qv : __longlong_as_double(0x7ff8000000000000LL);
   for (int i = p - 1; i >= 0; --i) {
     double t = w[i];
     for (int j = i + 1; j < p; ++j) t -= L[j * p + i] * w[j];
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(256) beta_max_kernel(int n, int p, int K, int 
   double best = -INFINITY;
   for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
     const int k = e / M, m = e - k * M;
-    if (status[k] != 0) continue;
+    if (status[k] != 0 && status[k] != 3) continue;  // NEG_RESID columns: qfull = NaN
     const double d = b - bha[e];
     const double q = fma(d * d, hia[k], qfull[e]);
     const double l = -0.5 * (nd * log(q) + logdetV[k] + c0) + (lambdas[m] - 1.0) * Sv;
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(256) sigma_lambda_kernel(int n, int K, int M, 
     slice_range(K * M, nsl, sl, lo, hi);
     for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
       const int k = e / M, m = e - k * M;
-      if (status[k] != 0) continue;
+      if (status[k] != 0 && status[k] != 3) continue;
       const double l = -0.5 * (qfull[e] * is2 + c1 + logdetV[k]) + (lambdas[m] - 1.0) * Sv;
       best = fmax(best, l);
     }
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(256) sigma_lambda_kernel(int n, int K, int M, 
     const double c0 = nd * (ln2pi + 1.0 - log(nd)), lt = (lambdas[m] - 1.0) * Sv;
     slice_range(K, nsl, sl, lo, hi);
     for (int k = lo + threadIdx.x; k < hi; k += blockDim.x) {
-      if (status[k] != 0) continue;
+      if (status[k] != 0 && status[k] != 3) continue;
       const double q = qfull[(size_t)k * M + m];
       const double l = -0.5 * (nd * log(q) + logdetV[k] + c0) + lt;
       best = fmax(best, l);

@@ -30,12 +30,34 @@ def test_reference_arm_line():
     assert d["config"]["workload"].startswith("C4")
 
 
+def test_gpus_n_starts_n_ranks():
+    """`bench.py --gpus 2` without a torchrun environment starts two ranks itself (through
+    torch.distributed.run on 127.0.0.1); they meet in one gloo group (--probe-ranks: the
+    launch check, no GPU work) and rank 0 alone prints the line."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--probe-ranks"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["world"] == 2 and sorted(d["ranks"]) == [0, 1] and sorted(d["local_ranks"]) == [0, 1]
+
+
+def test_gpus_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--probe-ranks"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("extra", [[], ["--dist"]])
+@pytest.mark.parametrize("extra", [[], ["--dist"], ["--scaling", "weak"]])
 def test_native_arm_line(extra):
     d = _run(["--points", "592", "--steps", "1", "--warmup", "3", "--no-cpu-baseline", *extra], timeout=900)
     assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
-    assert d["value"] > 0 and d["unit"] == "points/s" and d["dtype"] == "f64" and d["scaling"] == "weak"
+    assert d["value"] > 0 and d["unit"] == "points/s" and d["dtype"] == "f64"
+    assert d["scaling"] == ("weak" if "weak" in extra else "strong")
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1.0

@@ -426,6 +426,59 @@ def test_status_and_errors(orc):
     assert orc.validate(coords[:3], y[:3], X[:3], [good], [0.5]) == -1
 
 
+def test_xvx_not_pd_constructed(orc):
+    """Step 5: the constructed X of tests/constructed.py passes the full-rank check
+    but XᵀV⁻¹X (V = I exactly) is singular in FP64 — pinned by exact rational arithmetic,
+    not by the oracle: the exact Gram matrix is PD, yet its FP64 entries are exactly n."""
+    from fractions import Fraction
+    import constructed
+    coords, y, X, P, lam, e = constructed.xvx_singular()
+    n = X.shape[0]
+    x2 = [Fraction(float(v)) for v in X[:, 1]]
+    g12, g22 = sum(x2), sum(v * v for v in x2)
+    assert g12 == n and g22 - n == Fraction(int((e * e).sum()), 2 ** 60)  # det = n·2⁻⁶⁰Σe² > 0
+    acc = 0.0
+    for v in X[:, 1]:  # the FP64 left-to-right sum of x2·x2 (any order gives the same)
+        acc += v * v
+    assert acc == float(n) and float(np.sum(X[:, 1] * X[:, 1])) == float(n)
+    # ρ underflows to exactly 0 off the diagonal: V = I
+    for w in P:
+        V = orc.build_V(coords, w)
+        assert np.array_equal(V, np.eye(n))
+    assert orc.validate(coords, y, X, P, lam) == 0  # not ERANK
+    out = orc.eval_batch(coords, y, X, P, lam, summaries=True)
+    assert np.all(out["status"] == 2)
+    assert np.all(np.isneginf(out["loglik"])) and np.all(np.isnan(out["betahat"]))
+    assert np.all(np.isnan(out["logdetV"])) and np.all(np.isnan(out["sigma2hat"]))
+
+
+def test_neg_resid_constructed(orc):
+    """Step 8 and R12: y' of the λ = 1 column lies in span(X) (tests/constructed.py),
+    so Eq. 4's q vanishes up to Box-Cox rounding and Step 8's subtraction is noise: that
+    column fails (status NEG_RESID, ℓ_p = −∞, σ̂² and β̂ NaN), the λ = 0.5 column stands."""
+    import constructed
+    coords, y, X, P, lam = constructed.resid_in_span()
+    out = orc.eval_batch(coords, y, X, P, lam, summaries=True)
+    assert np.all(out["status"] == 3)
+    yy = out["ssqYX"][:, 0, 0]
+    assert np.all(np.abs(out["ssqResidual"][:, 0]) <= 1e-13 * yy)
+    assert np.all(np.isneginf(out["loglik"][:, 0])) and np.all(np.isnan(out["sigma2hat"][:, 0]))
+    assert np.all(np.isnan(out["betahat"][:, 0])) and np.all(np.isneginf(out["loglik_reml"][:, 0]))
+    # the other column: finite, and Step 8 agrees with the direct Eq. 4 form
+    assert np.all(np.isfinite(out["loglik"][:, 1])) and np.all(out["sigma2hat"][:, 1] > 0)
+    q8, q4 = out["ssqResidual"][:, 1], out["qdirect"][:, 1]
+    assert np.all(q4 > 1e-6 * out["ssqYX"][:, 1, 1])
+    assert np.abs(q8 - q4).max() <= 1e-9 * q4.min()
+    # log|V| and the Table-1 summaries of a NEG_RESID point stay valid
+    assert np.all(np.isfinite(out["logdetV"])) and np.all(np.isfinite(out["ssqYX"]))
+    # the profiles use the valid column only (R12): λ-profile of column 0 is −∞
+    grid = np.linspace(-1.0, 4.0, 5).reshape(1, -1).repeat(X.shape[1], 0)
+    pb, ps, pl = orc.profiles(X.shape[0], X.shape[1], out["ssqYX"], out["logdetV"], out["status"], lam, y,
+                              grid, np.array([0.5, 1.0]))
+    assert np.isneginf(pl[0]) and pl[1] == pytest.approx(out["loglik"][:, 1].max(), rel=1e-12)
+    assert np.all(np.isfinite(pb)) and np.all(np.isfinite(ps))
+
+
 def test_thread_determinism(orc):
     coords, y, X, P, lam = synthgen.make_inputs("C2", K=16)
     a = orc.eval_batch(coords, y, X, P, lam, nthreads=1)
