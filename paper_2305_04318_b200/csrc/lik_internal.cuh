@@ -81,6 +81,7 @@ inline SlotGeom make_geom(int n, int r) {
 enum { MODE_BESSEL = 0, MODE_GAUSS = 1, MODE_BAD = 2 };
 struct PointConst {
   double cX, sX, sY, cY;   // u/φX = cX hx − sX hy,  v/φY = sY hx + cY hy
+  double qX, qS, qT, qY;   // the same rows scaled by √(8κ): s = z² = (qX hx − qS hy)² + (qT hx + qY hy)²
   double kappa;            // κ
   double eightk;           // 8κ (s = z² = 8κ d², exact)
   double inv4k;            // 1/(4κ)  (the Gamma-mixture quadrature, matern_rho.cuh)
@@ -91,13 +92,14 @@ struct PointConst {
   int olo, ohi;            // table octaves built for this point (its range of s ± 1 octave)
 };
 
-// Per-point Chebyshev table of ln ρ on binary octaves of s = z² = 8κ·d² ∈ [2^e,
+// Per-point Chebyshev table of log2 ρ on binary octaves of s = z² = 8κ·d² ∈ [2^e,
 // 2^{e+1}), e = CHEB_ELO .. CHEB_ELO + CHEB_NOCT − 1 (the build needs no square
-// root).  Each interval (CHEB_SUB per octave) stores CHEB_STRIDE doubles: a base
-// H, one pad (so the coefficients are 16-byte aligned), then the CHEB_N monomial
-// coefficients (in t ∈ [−1, 1), an exact power-of-two map of s) of the degree
-// CHEB_N − 1 Chebyshev interpolant of h(s) = ln ρ(√s) − H, so that ln ρ = H + h(s).
-// Below 2^CHEB_ELO the exact evaluation is used; at and above 2^e_zero ρ = 0.
+// root).  Each interval (CHEB_SUB per octave) stores CHEB_N doubles (16-byte aligned
+// pairs, then 2 pad doubles): the monomial coefficients, in t ∈ [−1, 1) (an exact power-of-two map of s),
+// of the degree CHEB_N − 1 Chebyshev interpolant of log2 ρ(√s) (base 2, so the build's
+// exp is a plain 2^y).  Below 2^CHEB_ELO the exact evaluation is used; at and above
+// 2^e_zero ρ = 0: the interval of the octave e_zero holds the constant −2000 (2^−2000
+// flushes to 0), and the build clamps every larger s to it.
 // Two table layouts, chosen per call from n (cheb_sub_for): SUB = 1 whole octaves
 // with degree 19; SUB = 2 splits every octave at its linear midpoint ([1, 1.5) and
 // [1.5, 2) × 2^e; interval = SUB·octave + the top mantissa bit of s) with degree
@@ -111,6 +113,9 @@ template <int SUB>
 struct Cheb {
   static_assert(SUB == 1 || SUB == 2, "intervals per octave");
   static constexpr int N = SUB == 1 ? 20 : 16;  // coefficients per interval
+  // + 2 pad doubles: consecutive intervals start 16 bytes (4 banks) apart, so lanes of a
+  // warp reading the same pair of different intervals hit different banks (a stride of
+  // a multiple of 128 bytes serialises them: build 1.6× slower, measured)
   static constexpr int STRIDE = N + 2;
   static constexpr int NINT = CHEB_NOCT * SUB;  // intervals
   static constexpr int TABLE_D = STRIDE * NINT;

@@ -89,6 +89,11 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
   P.sX = s / phiX;
   P.sY = s / phiY;
   P.cY = c / phiY;
+  const double r8k = sqrt(8.0 * kappa);
+  P.qX = r8k * P.cX;
+  P.qS = r8k * P.sX;
+  P.qT = r8k * P.sY;
+  P.qY = r8k * P.cY;
   P.kappa = kappa;
   P.eightk = 8.0 * kappa;
   P.inv4k = 0.25 / kappa;
@@ -317,17 +322,20 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
     cheb[idx] = cc;
   }
   __syncthreads();
+  // monomial coefficients of log2 ρ = log2(e)·(line + Σ c_j T_j(t)); the octave e_zero
+  // (if built) holds the constant −2000, which the build's 2^y flushes to 0
   double* T = table + (size_t)blockIdx.x * TABLE_D;
+  constexpr double kLog2e = 1.4426950408889634074;
   for (int idx = olo * CHEB_SUB * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_STRIDE; idx += 256) {
-    const int iv = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE - 2;
+    const int iv = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE;
     double a = 0.0;
     if (CHEB_ELO + iv / CHEB_SUB < ez) {
-      if (kk == -2) {
-        a = 0.5 * (edge[iv] + edge[iv + 1]);  // H: the line's value at t = 0
-      } else if (kk >= 0) {
-        for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[iv * CHEB_N + jj] * tco[jj * CHEB_N + kk];
-        if (kk == 1) a += 0.5 * (edge[iv + 1] - edge[iv]);  // the line's slope in t
-      }
+      for (int jj = CHEB_N - 1; jj >= kk; --jj) a += cheb[iv * CHEB_N + jj] * tco[jj * CHEB_N + kk];
+      if (kk == 0) a += 0.5 * (edge[iv] + edge[iv + 1]);  // the line's value at t = 0
+      if (kk == 1) a += 0.5 * (edge[iv + 1] - edge[iv]);  // the line's slope in t
+      a *= kLog2e;
+    } else if (kk == 0) {
+      a = -2000.0;
     }
     T[idx] = a;
   }
@@ -367,24 +375,28 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
                                                     const double* __restrict__ table,
                                                     const double* __restrict__ Bt,
                                                     double* __restrict__ ws) {
-  constexpr int CHEB_SUB = SUB, CHEB_STRIDE = Cheb<SUB>::STRIDE, TABLE_D = Cheb<SUB>::TABLE_D;
+  constexpr int CHEB_STRIDE = Cheb<SUB>::STRIDE, TABLE_D = Cheb<SUB>::TABLE_D;
   const int slot = blockIdx.y;
   const PointConst P = pc[k0 + slot];
   if (P.mode == MODE_BAD) return;
   const int npad = g.nt * TB;
-  __shared__ double sx[2][TB], sy[2][TB];
+  __shared__ __align__(16) double2 sxy[2][TB];  // (x, y) of the tile's row and column sites
   __shared__ __align__(16) double coef[TABLE_D];
   __shared__ double etab[16];
   if (threadIdx.x < 16) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  // octaves [olo, oz] of the table; oz = the underflow octave (constant −2000) if built
+  const int ezo = P.e_zero - CHEB_ELO;
+  const int olo = P.olo, oz = max(olo, min(P.ohi, ezo));
+  const unsigned span = ezo <= P.ohi ? 0x7fffffffu : (unsigned)(P.ohi - olo);
   if (P.mode == MODE_BESSEL) {
-    const double* src = table + (size_t)slot * TABLE_D;
-    const int oend = min(P.ohi + 1, max(P.olo, P.e_zero - CHEB_ELO));  // octaves [olo, oend)
-    for (int e = P.olo * CHEB_SUB * CHEB_STRIDE + threadIdx.x; e < oend * CHEB_SUB * CHEB_STRIDE; e += 256)
-      coef[e] = src[e];
+    const double2* src = reinterpret_cast<const double2*>(table + (size_t)slot * TABLE_D);
+    double2* dst = reinterpret_cast<double2*>(coef);
+    for (int e = olo * SUB * CHEB_STRIDE / 2 + threadIdx.x; e < (oz + 1) * SUB * CHEB_STRIDE / 2; e += 256)
+      dst[e] = src[e];
   }
   // thread -> column c, rows r0 + 4q (q < 16): a warp covers 32 consecutive
-  // columns of one row; with Morton-ordered sites their z values mostly share an
-  // octave, so the coefficient loads are shared-memory broadcasts.
+  // columns of one row; with Morton-ordered sites their s values mostly share an
+  // interval, so the coefficient loads are shared-memory broadcasts.
   const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
   for (int tt = 0; tt < BUILD_TILES; ++tt) {
     const int tile = blockIdx.x * BUILD_TILES + tt;
@@ -404,18 +416,16 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
     while (tri_index(i, 0) > tile) --i;
     const int j = tile - tri_index(i, 0);
     __syncthreads();  // previous tile's coordinates are no longer read
-    if (threadIdx.x < TB) {
-      const int gi = i * TB + threadIdx.x;
-      sx[0][threadIdx.x] = gi < g.n ? coords[2 * gi] : 0.0;
-      sy[0][threadIdx.x] = gi < g.n ? coords[2 * gi + 1] : 0.0;
-    } else if (threadIdx.x < 2 * TB) {
-      const int gj = j * TB + threadIdx.x - TB;
-      sx[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj] : 0.0;
-      sy[1][threadIdx.x - TB] = gj < g.n ? coords[2 * gj + 1] : 0.0;
+    if (threadIdx.x < 2 * TB) {
+      const int side = threadIdx.x >> 6, l = threadIdx.x & 63;
+      const int gi = (side ? j : i) * TB + l;
+      sxy[side][l] = gi < g.n ? reinterpret_cast<const double2*>(coords)[gi] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const double xj = sx[1][c], yj = sy[1][c];
+    const double2 cj = sxy[1][c];
     const bool regular = (i > j) && ((i + 1) * TB <= g.n);
+    // the thread's 16 rows r0 + 4q share the swizzle of r0 (rows differ by multiples of 4)
+    double* Tc = T + sw_off(r0, c);
     unsigned slow = 0u;
     if (P.mode == MODE_BESSEL) {
 #pragma unroll 2
@@ -423,18 +433,19 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
         double hx[BUILD_NE], hy[BUILD_NE], v[BUILD_NE];
 #pragma unroll
         for (int e = 0; e < BUILD_NE; ++e) {
-          hx[e] = sx[0][r0 + 4 * (q + e)] - xj;
-          hy[e] = sy[0][r0 + 4 * (q + e)] - yj;
+          const double2 ri = sxy[0][r0 + 4 * (q + e)];
+          hx[e] = ri.x - cj.x;
+          hy[e] = ri.y - cj.y;
         }
-        matern_rho_tableN<BUILD_NE, SUB>(P, coef, etab, hx, hy, v, slow, q);
+        matern_rho_tableN<BUILD_NE, SUB>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
 #pragma unroll
-        for (int e = 0; e < BUILD_NE; ++e) T[sw_off(r0 + 4 * (q + e), c)] = v[e];
+        for (int e = 0; e < BUILD_NE; ++e) Tc[(q + e) * 4 * KC] = v[e];
       }
     } else {
 #pragma unroll 4
       for (int q = 0; q < 16; ++q) {
-        const int ra = r0 + 4 * q;
-        T[sw_off(ra, c)] = exp(-2.0 * aniso_d2(P, sx[0][ra] - xj, sy[0][ra] - yj));
+        const double2 ri = sxy[0][r0 + 4 * q];
+        Tc[q * 4 * KC] = exp(-2.0 * aniso_d2(P, ri.x - cj.x, ri.y - cj.y));
       }
     }
     if (!regular || slow) {
@@ -451,7 +462,8 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
         } else if (i == j && c > r) {
           v = 0.0;
         } else if ((slow >> q) & 1u) {
-          v = matern_rho_exact(P, sx[0][r] - xj, sy[0][r] - yj);
+          const double2 ri = sxy[0][r];
+          v = matern_rho_exact(P, ri.x - cj.x, ri.y - cj.y);
         } else {
           continue;
         }

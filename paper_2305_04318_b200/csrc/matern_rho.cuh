@@ -124,85 +124,74 @@ static __constant__ double kExp2Tab[16] = {
     1.4142135623730951, 1.4768261459394993, 1.5422108254079407, 1.6104903319492543,
     1.681792830507429, 1.7562521603732995, 1.8340080864093424, 1.9152065613971474};
 
-// exp(x) for x ≤ 1 (the table path's ρ = exp(ln ρ), ln ρ ≤ 0; x < −760 is clamped there,
-// where the result underflows to 0 — ln ρ reaches far below −746 inside the last
-// non-zero octave for large κ): k = rint(16x/ln 2), r = x − k ln2/16 (Cody-Waite, the
-// high part of ln2/16 has 32 significant bits so k·hi is exact for |k| < 2^21),
-// e^r − 1 by its degree-7 Taylor polynomial (|r| ≤ ln2/32: truncation < 2e-18),
-// e^x = 2^(k>>4) · T[k & 15] · (1 + q), the power of two applied in two exact halves
-// so subnormal results are rounded once.  etab = kExp2Tab copied to shared memory.
-// ≤ 1 ulp (checked against mpmath over [−746, 1]).
-__device__ __forceinline__ double exp_neg(double x, const double* etab) {
+// 2^y for y ≤ ~0 (the table path's ρ = 2^{log2 ρ}): k = rint(16y), r = y − k/16 (exact,
+// |r| ≤ 1/32), 2^r − 1 = Σ_{j=1..7} (r ln 2)^j / j! (truncation < 2e-18), 2^y =
+// 2^(k>>4) · T[k & 15] · (1 + q) with T[j] = 2^(j/16) (etab, shared memory), the power
+// of two added to the exponent field.  Results below 2^−1021 (ρ < 4.5e-308, R8) are
+// flushed to 0 — so is the −2000 of the table's underflow octave.  ≤ 1 ulp.
+__device__ __forceinline__ double exp2_neg(double y, const double* etab) {
   const double shift = 6755399441055744.0;  // 1.5·2^52: round-to-nearest integer in the low bits
-  x = fmax(x, -760.0);  // keeps both 2^(m/2) factors normal; the product underflows to 0
-  const double kds = fma(x, 23.083120654223414, shift);
+  const double kds = fma(y, 16.0, shift);
   const double kd = kds - shift;
   const int k = __double2loint(kds);
-  double r = fma(kd, -0.04332169877307024, x);
-  r = fma(kd, -1.1926343307941173e-11, r);
-  double q = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
-  q = fma(q, r, 1.0 / 120.0);
-  q = fma(q, r, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
+  const double r = fma(kd, -0.0625, y);
+  double q = fma(r, 1.5252733804059840e-05, 1.5403530393381608e-04);  // (ln2)^7/7!, (ln2)^6/6!
+  q = fma(q, r, 1.3333558146428443e-03);
+  q = fma(q, r, 9.6181291076284772e-03);
+  q = fma(q, r, 5.5504108664821580e-02);
+  q = fma(q, r, 2.4022650695910071e-01);
+  q = fma(q, r, 6.9314718055994531e-01);
   q *= r;
   const double tj = etab[k & 15];
-  const double v = fma(tj, q, tj);
+  const double v = fma(tj, q, tj);  // ∈ [0.97, 1.97]
   const int m = k >> 4;
-  // v ∈ [0.98, 2.04]: for m ≥ −1021 the result is normal and v·2^m is exactly v with
-  // m added to its exponent field (an integer add instead of two FP64 multiplies;
-  // bitwise the same result); below, the two-step scale rounds a subnormal once
-  if (m >= -1021) return __longlong_as_double(__double_as_longlong(v) + ((long long)m << 52));
-  const int m1 = m >> 1, m2 = m - m1;
-  const double s1 = __hiloint2double((m1 + 1023) << 20, 0), s2 = __hiloint2double((m2 + 1023) << 20, 0);
-  return (v * s1) * s2;
+  const double out = __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
+  return m >= -1021 ? out : 0.0;
 }
 
-// NE table evaluations interleaved (independent Horner chains for ILP).  Elements
-// that need the exact path (s = z² outside the point's table, or 0) set bit
-// `bit + e` of `slow`; their returned value is meaningless.
+// Table evaluation of NE elements, interleaved (independent Horner chains for ILP).
+// s = z² from the point's scaled rotation (no square root); the octave o of s is
+// clamped to [olo, oz] (oz: the underflow octave, or ohi); elements whose octave lies
+// outside [olo, ohs] (ohs = ohi, or "none" when the table reaches the underflow octave)
+// need the exact path and set bit `bit + e` of `slow` (s = 0 among them); their
+// returned value is meaningless.
 template <int NE, int SUB>
 __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const double* coef,
-                                                  const double* etab, const double (&hx)[NE],
-                                                  const double (&hy)[NE], double (&v)[NE],
-                                                  unsigned& slow, int bit) {
-  constexpr int CHEB_SUB = SUB, CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
-  double sv[NE], t[NE], h[NE];
-  int oc[NE];
-  bool zero[NE], in[NE];
+                                                  const double* etab, int olo, int oz, unsigned span,
+                                                  const double (&hx)[NE], const double (&hy)[NE],
+                                                  double (&v)[NE], unsigned& slow, int bit) {
+  constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
+  double t[NE], h[NE];
+  const double2* cp[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    sv[e] = P.eightk * aniso_d2(P, hx[e], hy[e]);  // s = z² (no square root)
-    const int ex = (int)((__double_as_longlong(sv[e]) >> 52) & 0x7ff) - 1023;
-    const int o = ex - CHEB_ELO;
-    zero[e] = ex >= P.e_zero;
-    in[e] = o >= P.olo && o <= P.ohi;
-    oc[e] = min(max(o, P.olo), P.ohi);
-    const int part = CHEB_SUB == 1 ? 0 : (int)((__double_as_longlong(sv[e]) >> 51) & 1);
-    t[e] = sv[e] * __longlong_as_double((long long)(1023 + CHEB_SUB - (oc[e] + CHEB_ELO)) << 52) -
-           (double)(2 * CHEB_SUB + 1 + 2 * part);
-    oc[e] = oc[e] * CHEB_SUB + part;  // from here on: the interval
+    const double u = fma(P.qX, hx[e], -P.qS * hy[e]);
+    const double w = fma(P.qT, hx[e], P.qY * hy[e]);
+    const double sv = fma(u, u, w * w);  // s = z² = 8κ d²
+    const int hi = __double2hiint(sv);
+    const int o = (hi >> 20) - (1023 + CHEB_ELO);
+    slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
+    const int oc = min(max(o, olo), oz);
+    const int part = SUB == 1 ? 0 : (hi >> 19) & 1;
+    const double scale = __hiloint2double((1023 + SUB - CHEB_ELO - oc) << 20, 0);
+    t[e] = fma(sv, scale, SUB == 1 ? -3.0 : (part ? -7.0 : -5.0));
+    cp[e] = reinterpret_cast<const double2*>(coef + (oc * SUB + part) * CHEB_STRIDE);
   }
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const double2 u = reinterpret_cast<const double2*>(coef + oc[e] * CHEB_STRIDE + 2)[CHEB_N / 2 - 1];
+    const double2 u = cp[e][CHEB_N / 2 - 1];
     h[e] = fma(u.y, t[e], u.x);
   }
 #pragma unroll
   for (int mm = CHEB_N / 2 - 2; mm >= 0; --mm) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      const double2 u = reinterpret_cast<const double2*>(coef + oc[e] * CHEB_STRIDE + 2)[mm];
+      const double2 u = cp[e][mm];
       h[e] = fma(fma(h[e], t[e], u.y), t[e], u.x);
     }
   }
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const double r = exp_neg(coef[oc[e] * CHEB_STRIDE] + h[e], etab);
-    v[e] = zero[e] ? 0.0 : r;
-    slow |= (unsigned)(!zero[e] && !(in[e] && sv[e] > 0.0)) << (bit + e);
-  }
+  for (int e = 0; e < NE; ++e) v[e] = exp2_neg(h[e], etab);
 }
 
 }  // namespace lik
