@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblik.so")
-SOURCES = ["lik_api.cpp", "matern_build.cu", "chol_fused.cu", "profiles.cu"]
-HEADERS = ["lik_internal.cuh", "matern_rho.cuh"]
+SOURCES = ["lik_api.cpp", "matern_build.cu", "chol_fused.cu", "chol_small.cu", "profiles.cu"]
+HEADERS = ["lik_internal.cuh", "matern_rho.cuh", "point_epilogue.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

@@ -41,6 +41,7 @@
 #include <cstdio>
 #include "../../include/lik.h"
 #include "lik_internal.cuh"
+#include "point_epilogue.cuh"
 
 #ifdef LIK_PHASE_TIMERS
 __device__ unsigned long long g_lik_phase[16];
@@ -824,26 +825,7 @@ __device__ int potrf_tail(double* S, int v, double tol, double* dlog, int* flag,
 }
 
 __device__ void write_point_failure(const CholArgs& A, int k, int code) {
-  const int tid = threadIdx.x;
-  const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  for (int e = tid; e < A.M; e += NT) {
-    A.loglik[(size_t)k * A.M + e] = -INFINITY;
-    A.sigma2hat[(size_t)k * A.M + e] = nan;
-    if (A.ssqBetahat) A.ssqBetahat[(size_t)k * A.M + e] = nan;
-    if (A.ssqResidual) A.ssqResidual[(size_t)k * A.M + e] = nan;
-    if (A.loglik_reml) A.loglik_reml[(size_t)k * A.M + e] = -INFINITY;
-    if (A.sigma2hat_reml) A.sigma2hat_reml[(size_t)k * A.M + e] = nan;
-  }
-  if (A.ssqYX) {
-    const int r = A.M + A.p;
-    for (int e = tid; e < r * r; e += NT) A.ssqYX[(size_t)k * r * r + e] = nan;
-  }
-  if (A.detReml && tid == 0) A.detReml[k] = nan;
-  for (int e = tid; e < A.M * A.p; e += NT) A.betahat[(size_t)k * A.M * A.p + e] = nan;
-  if (tid == 0) {
-    A.logdetV[k] = nan;
-    A.status[k] = code;
-  }
+  point_failure(A, k, code, threadIdx.x, NT);
 }
 
 #ifndef LIK_MIN_BLOCKS
@@ -873,7 +855,7 @@ __global__ void LIK_CHOL_BOUNDS chol_fused_kernel(CholArgs A) {
   const bool mine_b = sel == 1;
   const int k = A.k0 + blockIdx.x;
   const SlotGeom g = A.g;
-  const int nt = g.nt, M = A.M, p = A.p, r = g.r;
+  const int nt = g.nt, r = g.r;
   double* ws = A.ws + (size_t)blockIdx.x * g.slot_d;
   const int mode = A.pc[k].mode;
   const double nugget = A.pc[k].nugget;
@@ -1032,97 +1014,7 @@ __global__ void LIK_CHOL_BOUNDS chol_fused_kernel(CholArgs A) {
     Cm[a * 64 + b] = MG ? -staging[sw_off(g.off + max(a, b), g.off + min(a, b))] : staging[sw_off(a, b)];
   }
   __syncthreads();
-  if (A.ssqYX)
-    for (int e = tid; e < r * r; e += NT) A.ssqYX[(size_t)k * r * r + e] = Cm[(e / r) * 64 + e % r];
-  if (tid == LEAD_TID) {
-    double xmax = 0.0;
-    for (int a = 0; a < p; ++a) xmax = fmax(xmax, Cm[(M + a) * 64 + (M + a)]);
-    const double tolp = p * DBL_EPSILON * xmax;
-    int bad = 0;
-    for (int c = 0; c < p && !bad; ++c) {
-      double d = Cm[(M + c) * 64 + (M + c)];
-      for (int kk = 0; kk < c; ++kk) d -= Q[c * 64 + kk] * Q[c * 64 + kk];
-      if (!(d > tolp)) {
-        bad = 1;
-        break;
-      }
-      const double l = sqrt(d);
-      Q[c * 64 + c] = l;
-      for (int i = c + 1; i < p; ++i) {
-        double s = Cm[(M + i) * 64 + (M + c)];
-        for (int kk = 0; kk < c; ++kk) s -= Q[i * 64 + kk] * Q[c * 64 + kk];
-        Q[i * 64 + c] = s / l;
-      }
-    }
-    flag[1] = bad;
-    scal[1] = logdet;  // log|V| = Σ log pivots (Step 2)
-    double ldx = 0.0;  // log|XᵀV⁻¹X| = 2 Σ log Q_cc (Step 5, Table 1 detReml)
-    if (!bad)
-      for (int c = 0; c < p; ++c) ldx += 2.0 * log(Q[c * 64 + c]);
-    scal[2] = ldx;
-  }
-  __syncthreads();
-  if (flag[1]) {
-    write_point_failure(A, k, LIK_PT_XVX_NOT_PD);
-    return;
-  }
-  const double S = *A.S;
-  const double n = (double)g.n;
-  const double ldV = scal[1], ldx = scal[2];
-  const double ln2pi = 1.8378770664093454836;
-  const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  for (int m = tid; m < M; m += NT) {
-    double cv[64], bt[64];
-    double sb = 0.0;
-    for (int a = 0; a < p; ++a) {  // Step 6: c = Q⁻¹ XᵀV⁻¹y'
-      double s = Cm[(M + a) * 64 + m];
-      for (int b = 0; b < a; ++b) s -= Q[a * 64 + b] * cv[b];
-      cv[a] = s / Q[a * 64 + a];
-      sb += cv[a] * cv[a];  // Step 7: ssqBetahat = cᵀc
-    }
-    const double yy = Cm[m * 64 + m];
-    const double q = yy - sb;  // Step 8: ssqResidual
-    // R12: the subtraction resolves q only when q > 1e-10·yy; otherwise the λ
-    // column fails (ℓ_p = −∞, σ̂²/β̂ NaN, status NEG_RESID) — no OK column can
-    // report q ≤ 0 (log σ̂² = −∞ would make ℓ_p = +∞)
-    const bool neg = !(q > 1e-10 * yy);
-    for (int a = p - 1; a >= 0; --a) {  // β̂ = Q⁻ᵀ c (Eq. betahat)
-      double s = cv[a];
-      for (int b = a + 1; b < p; ++b) s -= Q[b * 64 + a] * bt[b];
-      bt[a] = s / Q[a * 64 + a];
-    }
-    const size_t km = (size_t)k * M + m;
-    if (A.ssqBetahat) A.ssqBetahat[km] = sb;
-    if (A.ssqResidual) A.ssqResidual[km] = yy - sb;
-    if (neg) {
-      A.loglik[km] = -INFINITY;
-      A.sigma2hat[km] = nan;
-      for (int a = 0; a < p; ++a) A.betahat[km * p + a] = nan;
-      if (A.loglik_reml) A.loglik_reml[km] = -INFINITY;
-      if (A.sigma2hat_reml) A.sigma2hat_reml[km] = nan;
-      atomicExch(&flag[2], 1);
-    } else {
-      const double s2 = q / n;  // Eq. 4
-      const double jac = (A.lambdas[m] - 1.0) * S;
-      // Eq. (profile): −2ℓ_p = n log σ̂² + log|V| − 2(λ−1)Σ log y + n log 2π + n
-      A.loglik[km] = -0.5 * (n * log(s2) + ldV + n * ln2pi + n) + jac;
-      A.sigma2hat[km] = s2;
-      for (int a = 0; a < p; ++a) A.betahat[km * p + a] = bt[a];
-      if (A.loglik_reml || A.sigma2hat_reml) {
-        // Eq. remlpro with σ̂²_reml = q/(n−p) (Eq. sigmahat_reml_y)
-        const double np_ = n - p, s2r = q / np_;
-        if (A.sigma2hat_reml) A.sigma2hat_reml[km] = s2r;
-        if (A.loglik_reml)
-          A.loglik_reml[km] = -0.5 * (np_ * log(s2r) + ldV + ldx + n * ln2pi + np_) + jac;
-      }
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    if (A.detReml) A.detReml[k] = ldx;
-    A.logdetV[k] = ldV;
-    A.status[k] = flag[2] ? LIK_PT_NEG_RESID : LIK_PT_OK;
-  }
+  point_epilogue(A, k, Cm, 64, Q, 64, logdet, flag, scal, tid, NT, LEAD_TID);
   PH(8);
   PH_FLUSH();
 #ifdef LIK_CTA_TRACE

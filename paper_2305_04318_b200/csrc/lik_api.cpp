@@ -47,6 +47,7 @@ struct lik_ctx {
   char* io = nullptr;
   size_t io_bytes = 0;
   int wave_points = 0;
+  bool force_fused = std::getenv("LIK_NO_SMALL") != nullptr;  // A/B: keep chol_fused for small n
   // free-memory query of the last call (cudaMemGetInfo costs 0.1-5 ms of host time):
   // a call with the same K and slot size reuses it, so it gets the same wave size
   // and the workspace it already holds
@@ -257,7 +258,10 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   Nvtx nv_call("lik.eval");
   CUDA_TRY(c, after_previous(c, st));
   const SlotGeom g = lik::make_geom(n, M + p);
-  const size_t slot_bytes = g.slot_d * sizeof(double);
+  // small augmented matrices take chol_small (build + factor in one kernel, the matrix in
+  // shared memory): no workspace slot; a wave is bounded only by the table buffer
+  const bool small = !c->force_fused && lik::small_path_fits(n, M + p, p);
+  const size_t slot_bytes = small ? (size_t)lik::TABLE_D * sizeof(double) : g.slot_d * sizeof(double);
   // Wave size W (points per table/build/chol launch).  All CTAs of a chol launch
   // start together and the launch ends with its slowest point, so fewer, larger
   // launches lose less to that tail (the CTA scheduler backfills within a launch):
@@ -299,6 +303,10 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     if (W < 1) {
       c->avail_K = -1;
       return fail(c, LIK_ENOMEM, "one workspace slot (%zu bytes) exceeds free HBM", slot_bytes);
+    }
+    if (small) {
+      W = std::min(K, 65535);
+      break;
     }
     if ((rc = ensure(c, &c->ws, &c->ws_bytes, (size_t)W * slot_bytes)) == LIK_OK) break;
     cudaGetLastError();  // clear the allocation error
@@ -358,7 +366,8 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     {
       Nvtx nvb("lik.build");
       CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, k0, kw, c->table, S + 1, st));
-      CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
+      if (!small)
+        CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
     }
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
@@ -382,7 +391,10 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     a.loglik_reml = ex.loglik_reml;
     a.sigma2hat_reml = ex.sigma2hat_reml;
     Nvtx nvc("lik.chol");
-    CUDA_TRY(c, lik::launch_chol(a, kw, st));
+    if (small)
+      CUDA_TRY(c, lik::launch_chol_small(a, coords_p, bt, g.nt * lik::TB, c->table, kw, st));
+    else
+      CUDA_TRY(c, lik::launch_chol(a, kw, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
   }
   tr.mark("launches");
@@ -402,7 +414,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
       cudaEventElapsedTime(&ms, c->ev[3 + 2 * w], c->ev[4 + 2 * w]);
       c->stage_ms[LIK_STAGE_CHOL] += ms;
     }
-    c->stage_n[LIK_STAGE_BUILD] += 2 * nwaves;  // table + build
+    c->stage_n[LIK_STAGE_BUILD] += (small ? 1 : 2) * nwaves;  // table (+ build)
     c->stage_n[LIK_STAGE_CHOL] += nwaves;
   }
   return LIK_OK;

@@ -166,6 +166,11 @@ struct CholArgs {
   double* sigma2hat_reml;  // K×M
 };
 cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
+// chol_small.cu: the whole path for small augmented matrices in one kernel (no
+// workspace); small_path_fits says whether (n, r = M + p) takes it.
+bool small_path_fits(int n, int r, int p);
+cudaError_t launch_chol_small(const CholArgs& a, const double* coords, const double* Bt, int ldb,
+                              const double* table, int kw, cudaStream_t st);
 size_t chol_smem_bytes();
 int profile_slices(long long K, int M);                       // slices of the (k, m) range
 size_t profile_partials(int p, int G, int Sg, int M, int nsl);  // doubles of partial maxima

@@ -145,3 +145,32 @@ def test_calls_on_different_streams_are_ordered(ctx):
             assert np.array_equal(o1[key].cpu().numpy(), a[key], equal_nan=True), key
             assert np.array_equal(o2[key].cpu().numpy(), b[key], equal_nan=True), key
             assert np.array_equal(o3[key], a[key], equal_nan=True), key
+
+
+# --------------------------------------------------------------------------- small path
+@pytest.mark.parametrize("name,K", [("C1", 16), ("C2", 400), ("swiss", 300)])
+def test_small_path_matches_fused_path(name, K):
+    """chol_small (build + factor of the whole augmented matrix in shared memory, taken
+    for n_pad + r_pad ≤ 216) against chol_fused (64-tiles through HBM, LIK_NO_SMALL) on
+    the same inputs: two independent factorisations agree to rounding."""
+    if name == "swiss":  # the paper's Swiss-rainfall shape (P:582-585): n = 100, p = 2, M = 34
+        cfg = synthgen.Config("sw", 100, 2, K, 34, True, "uniform", "swiss-shaped")
+        coords, y, X = synthgen.make_dataset(cfg, seed=5)
+        P, lam = synthgen.make_params(cfg, K, seed=6), np.linspace(-1.0, 2.0, 34)
+    else:
+        coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
+    a = lik.create(0).eval_batch(coords, y, X, P, lam)
+    os.environ["LIK_NO_SMALL"] = "1"
+    try:
+        c = lik.create(0)
+    finally:
+        del os.environ["LIK_NO_SMALL"]
+    b = c.eval_batch(coords, y, X, P, lam)
+    c.close()
+    assert np.array_equal(a["status"], b["status"])
+    ok = a["status"] == 0
+    np.testing.assert_allclose(a["loglik"][ok], b["loglik"][ok], rtol=1e-11)
+    np.testing.assert_allclose(a["logdetV"][ok], b["logdetV"][ok], rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(a["sigma2hat"][ok], b["sigma2hat"][ok], rtol=1e-10)
+    sc = np.abs(b["betahat"][ok]).max(axis=-1, keepdims=True)
+    assert (np.abs(a["betahat"][ok] - b["betahat"][ok]) / sc).max() <= 1e-9
