@@ -14,15 +14,13 @@
 // to n_pad = 8⌈n/8⌉ with identity rows (log|V| and L⁻¹B unchanged); the r rows of Bᵀ
 // start at n_pad.
 //
-// Right-looking elimination, one 8-column tile column k per step, with lookahead:
-//   phase A (all warps):  L_ik = A_ik L_kk⁻ᵀ = S_ik (−W_k)ᵀ for the tiles below the
-//                         diagonal (W_k = L_kk⁻¹ from the previous phase);
-//   phase B: the lead warp updates tile (k+1, k+1), factors it in registers (one
-//            rsqrt per pivot, the 8 pivots the only serial chain) and inverts it
-//            (−W_{k+1}); the other warps update every other trailing tile,
-//            S_ij += L_ik L_jkᵀ, in row blocks of up to 4 tiles (L_ik reused).
-// Two CTA barriers per step.  The pivot chain of step k+1 runs beside the trailing
-// update of step k.
+// Right-looking elimination, one 8-column tile column k per step, with lookahead: a
+// panel group of four warps brings column k+1 up to date with column k, factors its
+// diagonal tile in registers (one rsqrt per pivot — the 8 pivots are the only serial
+// chain) and solves the column below it (L_i,k+1 = A_i,k+1 L_k+1,k+1⁻ᵀ = S (−W)ᵀ),
+// while the other warps apply column k to the columns ≥ k+2 (S_ij += L_ik L_jkᵀ, row
+// segments, four independent tiles at a time).  One CTA barrier per step: the pivot
+// chain and the solve of step k+1 run beside the trailing update of step k.
 #include <cfloat>
 #include <algorithm>
 #include <cstdint>
@@ -30,6 +28,17 @@
 #include "lik_internal.cuh"
 #include "matern_rho.cuh"
 #include "point_epilogue.cuh"
+
+#ifdef LIK_PHASE_TIMERS
+__device__ unsigned long long g_lik_small_phase[16];
+#define SPH_INIT() long long sph_t = clock64(); long long sph_acc[8] = {0}
+#define SPH(i) do { const long long t_ = clock64(); sph_acc[i] += t_ - sph_t; sph_t = t_; } while (0)
+#define SPH_FLUSH(w, slot) do { if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) == (w)) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_lik_small_phase[8 * (slot) + i_], (unsigned long long)sph_acc[i_]); } while (0)
+#else
+#define SPH_INIT() do {} while (0)
+#define SPH(i) do {} while (0)
+#define SPH_FLUSH(w, slot) do {} while (0)
+#endif
 
 namespace lik {
 namespace {
@@ -57,79 +66,56 @@ __device__ __forceinline__ double frag_ab(const double* X, int lane, int kk) {
   return X[toff(lane >> 2, 4 * kk + (lane & 3))];
 }
 
-// The lead warp: factor the 8×8 diagonal tile (stored as −A), one row per lane
-// (lanes 8-31 mirror lanes 0-7), and write −W = −L⁻¹ into Wn and the pivots into piv.
-// A pivot ≤ tol sets *bad.
+// The lead warp: factor the 8×8 diagonal tile (stored as −A) and write −W = −L⁻¹ into
+// Wn and the pivots into piv; a pivot ≤ tol sets *bad.  Every lane holds the whole lower
+// triangle (36 doubles, broadcast loads) and factors it redundantly: no shuffles, so the
+// only serial chain is rsqrt → scale → update of the next pivot (≈ 90 cycles per pivot;
+// the one-row-per-lane version with shuffles took ≈ 2,200 cycles per tile).  Lane l < 8
+// then forms column l of W by forward substitution and stores it.
 __device__ __forceinline__ void factor8(const double* Skk, double* Wn, double* piv, double tol,
                                         int* bad) {
   const int lane = threadIdx.x & 31, l = lane & 7;
-  double a[8];
+  double a[36];  // a[i(i+1)/2 + j] = A_ij, j ≤ i
 #pragma unroll
-  for (int m = 0; m < 8; ++m) a[m] = (m <= l) ? -Skk[toff(l, m)] : 0.0;
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) a[i * (i + 1) / 2 + j] = -Skk[toff(i, j)];
   int fail = 0;
-  double my_piv = 1.0, my_rinv = 1.0;
-  double piv_next = __shfl_sync(0xffffffffu, a[0], 0);
+  double rv[8], mypiv = 1.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const double pv = piv_next;
-    fail |= !(pv > tol);
-    const double rinv = rsqrt(pv);
-    if (l == c) {
-      a[c] = pv * rinv;
-      my_piv = pv;
-      my_rinv = rinv;
-    } else if (l > c) {
-      a[c] *= rinv;
-    }
-    if (c + 1 < 8) {  // the next pivot from lane c+1's own update, broadcast once
-      const double pn = a[c + 1] - a[c] * a[c];
-      piv_next = __shfl_sync(0xffffffffu, pn, c + 1);
-    }
+    const double d = a[c * (c + 1) / 2 + c];
+    fail |= !(d > tol);
+    const double r = rsqrt(d);
+    rv[c] = r;
+    if (l == c) mypiv = d;
+    a[c * (c + 1) / 2 + c] = d * r;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      if (m > c) {
-        const double lm = __shfl_sync(0xffffffffu, a[c], m);
-        if (l >= m) a[m] -= a[c] * lm;
-      }
-    }
+    for (int i = c + 1; i < 8; ++i) a[i * (i + 1) / 2 + c] *= r;
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i)
+#pragma unroll
+      for (int j = c + 1; j <= i; ++j) a[i * (i + 1) / 2 + j] -= a[i * (i + 1) / 2 + c] * a[j * (j + 1) / 2 + c];
   }
-  // column l of W = L⁻¹ by forward substitution (x = e_l)
+  // column l of W = L⁻¹: x_i = (δ_il − Σ_{m<i} L_im x_m) / L_ii
   double x[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = (i == l) ? 1.0 : 0.0;
-#pragma unroll
   for (int i = 0; i < 8; ++i) {
-    x[i] *= __shfl_sync(0xffffffffu, my_rinv, i);
+    double t = (i == l) ? 1.0 : 0.0;
 #pragma unroll
-    for (int m = 0; m < 8; ++m)
-      if (m > i) x[m] -= __shfl_sync(0xffffffffu, a[i], m) * x[i];
+    for (int m = 0; m < i; ++m) t -= a[i * (i + 1) / 2 + m] * x[m];
+    x[i] = t * rv[i];
   }
   if (lane < 8) {
 #pragma unroll
     for (int m = 0; m < 8; ++m) Wn[toff(m, l)] = -x[m];
-    piv[l] = my_piv;
+    piv[l] = mypiv;
   }
   if (lane == 0 && fail) *bad = 1;
 }
 
-// S_ij += L_ik L_jkᵀ for j = j0 .. j1 (one warp; L_ik's fragments reused)
-__device__ __forceinline__ void update_row(double* S, int i, int k, int j0, int j1, int lane) {
-  const double* Lik = S + tri8(i, k) * 64;
-  const double a0 = frag_ab(Lik, lane, 0), a1 = frag_ab(Lik, lane, 1);
-  const int co = toff(lane >> 2, 2 * (lane & 3));
-  for (int j = j0; j <= j1; ++j) {
-    const double* Ljk = S + tri8(j, k) * 64;
-    double* C = S + tri8(i, j) * 64;
-    double2 cv = *reinterpret_cast<const double2*>(C + co);
-    double c[2] = {cv.x, cv.y};
-    dmma8(c, a0, frag_ab(Ljk, lane, 0));
-    dmma8(c, a1, frag_ab(Ljk, lane, 1));
-    *reinterpret_cast<double2*>(C + co) = make_double2(c[0], c[1]);
-  }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
     chol_small_kernel(CholArgs A, SmallLayout Lt, const double* __restrict__ coords,
                       const double* __restrict__ Bt, int ldb, const double* __restrict__ table) {
   constexpr int NW = NT / 32, LEAD = NW - 1;
@@ -138,13 +124,14 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
   double* S = sm;
   double* coef = sm + Lt.off_tab;
   double2* sxy = reinterpret_cast<double2*>(sm + Lt.off_sites);
-  double* Wn = sm + Lt.off_w;  // two 8×8 tiles (−W, double-buffered by step parity)
+  double* Wn = sm + Lt.off_w;  // −W of the column being solved (8×8 tile)
   double* dlog = sm + Lt.off_dlog;
   double* scal = sm + Lt.off_misc;
   double* etab = scal + 8;
   int* flag = reinterpret_cast<int*>(etab + 16);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = A.k0 + blockIdx.x;
+  SPH_INIT();
   const PointConst P = A.pc[k];
   const int n = A.g.n, r = A.g.r, T = Lt.T, Tv = Lt.Tv;
   if (P.mode == MODE_BAD) {
@@ -165,99 +152,261 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
   if (tid < 4) flag[tid] = 0;
   __syncthreads();
 
-  // ---- Step 1: S = −A (lower tile triangle)
+  SPH(0);
+  // ---- Step 1: S = −A (lower tile triangle).  Each warp fills two tiles per pass (four
+  // independent table evaluations per lane: the chains of coefficient loads and FMAs
+  // overlap)
   const int ntile = T * (T + 1) / 2;
-  const int ea = lane >> 3, eb = lane & 7;  // this lane's elements (ea, eb) and (ea + 4, eb)
-  for (int t = warp; t < ntile; t += NW) {
-    int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while (tri8(I + 1, 0) <= t) ++I;
-    while (tri8(I, 0) > t) --I;
-    const int J = t - tri8(I, 0);
-    double* X = S + t * 64;
-    double v[2] = {0.0, 0.0};
-    if (I < Tv) {
-      const int j = 8 * J + eb;
-      double hx[2], hy[2];
+  const int ea = lane >> 3, eb = lane & 7;  // this lane's elements (ea, eb) and (ea + 4, eb) of a tile
+  for (int t0 = warp; t0 < ntile; t0 += 2 * NW) {
+    int I[2], J[2];
+    bool on[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int t = min(t0 + q * NW, ntile - 1);
+      on[q] = t0 + q * NW < ntile;
+      int ii = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+      while (tri8(ii + 1, 0) <= t) ++ii;
+      while (tri8(ii, 0) > t) --ii;
+      I[q] = ii;
+      J[q] = t - tri8(ii, 0);
+    }
+    double hx[4], hy[4], rho[4] = {0.5, 0.5, 0.5, 0.5};
+    unsigned slow = 0u;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = 8 * J[q] + eb;
       const double2 sj = j < n ? sxy[j] : make_double2(0.0, 0.0);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int i = 8 * I + ea + 4 * e;
+        const int i = 8 * I[q] + ea + 4 * e;
         const double2 si = i < n ? sxy[i] : make_double2(0.0, 0.0);
-        hx[e] = si.x - sj.x;
-        hy[e] = si.y - sj.y;
-      }
-      double rho[2];
-      unsigned slow = 0u;
-      if (P.mode == MODE_BESSEL) {
-        matern_rho_tableN<2, 1>(P, coef, etab, olo, oz, span, hx, hy, rho, slow, 0);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) rho[e] = exp(-2.0 * aniso_d2(P, hx[e], hy[e]));
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = 8 * I + ea + 4 * e;
-        if (i >= n || j >= n)
-          v[e] = (i == j) ? -1.0 : 0.0;
-        else if (j > i)
-          v[e] = 0.0;
-        else if (i == j)
-          v[e] = -(1.0 + P.nugget);
-        else
-          v[e] = ((slow >> e) & 1u) ? -matern_rho_exact(P, hx[e], hy[e]) : -rho[e];
-      }
-    } else if (J < Tv) {
-      const int j = 8 * J + eb;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int tr = 8 * (I - Tv) + ea + 4 * e;
-        v[e] = (tr < r && j < n) ? -Bt[(size_t)tr * ldb + j] : 0.0;
+        hx[2 * q + e] = si.x - sj.x;
+        hy[2 * q + e] = si.y - sj.y;
       }
     }
-    X[toff(ea, eb)] = v[0];
-    X[toff(ea + 4, eb)] = v[1];
+    const bool vtile = I[0] < Tv || I[1] < Tv;
+#ifdef LIK_SMALL_NO_RHO  // timing experiment only: results are wrong
+    if (false) {
+#else
+    if (vtile) {
+#endif
+      if (P.mode == MODE_BESSEL) {
+        matern_rho_tableN<4, 1>(P, coef, etab, olo, oz, span, hx, hy, rho, slow, 0);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) rho[e] = exp(-2.0 * aniso_d2(P, hx[e], hy[e]));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!on[q]) continue;
+      double* X = S + (t0 + q * NW) * 64;
+      const int j = 8 * J[q] + eb;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = 8 * I[q] + ea + 4 * e, x = 2 * q + e;
+        double v;
+        if (I[q] < Tv) {
+          if (i >= n || j >= n)
+            v = (i == j) ? -1.0 : 0.0;
+          else if (j > i)
+            v = 0.0;
+          else if (i == j)
+            v = -(1.0 + P.nugget);
+          else
+            v = ((slow >> x) & 1u) ? -matern_rho_exact(P, hx[x], hy[x]) : -rho[x];
+        } else {
+          const int tr = 8 * (I[q] - Tv) + ea + 4 * e;
+          v = (J[q] < Tv && tr < r && j < n) ? -Bt[(size_t)tr * ldb + j] : 0.0;
+        }
+        X[toff(ea + 4 * e, eb)] = v;
+      }
+    }
   }
   __syncthreads();
-
-  // ---- Steps 2-4: right-looking elimination of the Tv V tile columns
+  SPH(1);
+#ifdef LIK_SMALL_EXIT_AFTER_BUILD  // timing experiment only: results are wrong
+  if (tid < 1000000) return;
+#endif
+  // ---- Steps 2-4: right-looking elimination of the Tv V tile columns, two tile columns
+  // (a 16-column panel) per step: every trailing tile then takes 4 DMMAs per load and
+  // store of its accumulator (shared-memory traffic per DMMA −33 % against one column
+  // per step; with one column the updates saturated the shared-memory bandwidth and the
+  // lead's loads queued behind them).
+  // Roles by SM sub-partition (warp w issues on SMSP w mod 4): the lead (warp NW−1,
+  // SMSP 3) runs the pivot chain, whose dependent FP64 operations would otherwise queue
+  // behind other warps' DMMAs on the sub-partition's FP64 pipe (a DMMA-issuing
+  // neighbour on the same SMSP starves it completely, tools/phase0/chain_bench.cu); so no
+  // other warp of SMSP 3 issues DMMAs during the elimination.  G = the lead and warps
+  // NW−4..NW−2 (SMSPs 0-2): at step p they bring the next panel up to date with panel p,
+  // the lead factors its 16×16 diagonal block (two 8×8 tiles in registers, the solve and
+  // update between them by DMMA), and after a named barrier the other three solve the
+  // panel's rows below.  U = the warps below NW−4 on SMSPs 0-2: they apply panel p to
+  // the columns beyond the next panel.  One CTA barrier per step.
   const double tol = n * DBL_EPSILON * (1.0 + P.nugget);
-  if (warp == LEAD) factor8(S, Wn, dlog, tol, &flag[0]);
-  __syncthreads();
   const int co = toff(lane >> 2, 2 * (lane & 3));
-  for (int kc = 0; kc < Tv; ++kc) {
-    // phase A: L_ik = S_ik (−W_k)ᵀ, i > kc
-    const double* W = Wn + (kc & 1) * 64;
+  constexpr int NG = 4, NU = (NW - NG) / 4 * 3;
+  const bool in_g = warp >= NW - NG;
+  const int g = warp - (NW - NG);  // 0..3 in G; g = 3 is the lead
+  const bool in_u = !in_g && (warp & 3) != 3;
+  const int uw = (warp >> 2) * 3 + (warp & 3);  // U index 0..NU−1
+  double* Wa = Wn;
+  double* Wb = Wn + 64;
+  auto tile = [&](int i, int j) { return S + tri8(i, j) * 64; };
+  // X ← X (−W)ᵀ in place (the solve L_ij = A_ij L_jj⁻ᵀ with S = −A and Wn = −L_jj⁻¹)
+  auto solve_tile = [&](double* X, const double* W) {
+    const double x0 = frag_ab(X, lane, 0), x1 = frag_ab(X, lane, 1);
     const double w0 = frag_ab(W, lane, 0), w1 = frag_ab(W, lane, 1);
-    for (int i = kc + 1 + warp; i < T; i += NW) {
-      double* X = S + tri8(i, kc) * 64;
-      double c[2] = {0.0, 0.0};
-      dmma8(c, frag_ab(X, lane, 0), w0);
-      dmma8(c, frag_ab(X, lane, 1), w1);
+    double c[2] = {0.0, 0.0};
+    dmma8(c, x0, w0);
+    dmma8(c, x1, w1);
+    __syncwarp();
+    *reinterpret_cast<double2*>(X + co) = make_double2(c[0], c[1]);
+    __syncwarp();
+  };
+  // C += L_a Lbᵀ (one 8×8 product, two DMMAs)
+  auto upd_tile = [&](double* C, const double* La, const double* Lb) {
+    const double a0 = frag_ab(La, lane, 0), a1 = frag_ab(La, lane, 1);
+    const double b0 = frag_ab(Lb, lane, 0), b1 = frag_ab(Lb, lane, 1);
+    const double2 cv = *reinterpret_cast<const double2*>(C + co);
+    double c[2] = {cv.x, cv.y};
+    dmma8(c, a0, b0);
+    dmma8(c, a1, b1);
+    *reinterpret_cast<double2*>(C + co) = make_double2(c[0], c[1]);
+    __syncwarp();
+  };
+  auto g_bar = []() { asm volatile("bar.sync 1, %0;" ::"n"(NG * 32) : "memory"); };
+  // G, part 2 for the panel starting at column a (a < Tv): the lead factors the
+  // diagonal block; after the named barrier the other G warps solve rows ≥ a + 2
+  auto g_factor_solve = [&](int a) {
+    const int b = a + 1;  // b < T always (the B rows follow the V rows)
+    // (a single-column panel, b ≥ Tv: column b is a Schur column and gets column a's
+    // contribution from the step loop with the rest of the panel's update)
+    if (g == NG - 1) {
+      factor8(tile(a, a), Wa, dlog + 8 * a, tol, &flag[0]);
       __syncwarp();
-      *reinterpret_cast<double2*>(X + co) = make_double2(c[0], c[1]);
+      solve_tile(tile(b, a), Wa);
+      if (b < Tv) {
+        upd_tile(tile(b, b), tile(b, a), tile(b, a));
+        factor8(tile(b, b), Wb, dlog + 8 * b, tol, &flag[0]);
+      }
     }
-    __syncthreads();
-    // phase B: trailing update S_ij += L_i,kc L_j,kcᵀ, kc < j ≤ i
-    if (kc + 1 < T) {
-      if (warp == LEAD) {
-        update_row(S, kc + 1, kc, kc + 1, kc + 1, lane);
-        if (kc + 1 < Tv) {
-          __syncwarp();
-          factor8(S + tri8(kc + 1, kc + 1) * 64, Wn + ((kc + 1) & 1) * 64, dlog + 8 * (kc + 1), tol,
-                  &flag[0]);
-        }
-      } else {
-        // rows i ≥ kc+2, columns kc+1..i in blocks of 4; unit u → warp u mod (NW−1)
-        int u = 0;
-        for (int i = kc + 2; i < T; ++i) {
-          for (int j0 = kc + 1; j0 <= i; j0 += 4, ++u) {
-            if (u % (NW - 1) != warp) continue;
-            update_row(S, i, kc, j0, min(j0 + 3, i), lane);
-          }
+    g_bar();
+    if (g < NG - 1) {
+      for (int i = a + 2 + g; i < T; i += NG - 1) {
+        solve_tile(tile(i, a), Wa);
+        if (b < Tv) {
+          upd_tile(tile(i, b), tile(i, a), tile(b, a));
+          solve_tile(tile(i, b), Wb);
         }
       }
     }
+  };
+  if (in_g) g_factor_solve(0);  // panel 0
+  __syncthreads();
+  SPH(2);
+  for (int c0 = 0; c0 < Tv; c0 += 2) {
+    const int c1 = c0 + 1;
+    const bool two = c1 < Tv;        // panel columns c0 (and c1)
+    const int a = c0 + (two ? 2 : 1);  // the next panel's first column
+    if (in_g) {
+      // (1) columns a, a+1 (those < T) += panel (c0, c1), rows ≥ column; the lead takes
+      // the diagonal block, the other G warps the rows ≥ a + 2
+      if (a < T) {
+        auto upd_panel = [&](int i, int j) {
+          upd_tile(tile(i, j), tile(i, c0), tile(j, c0));
+          if (two) upd_tile(tile(i, j), tile(i, c1), tile(j, c1));
+        };
+        if (g == NG - 1) {
+          upd_panel(a, a);
+          if (a + 1 < T) {
+            upd_panel(a + 1, a);
+            upd_panel(a + 1, a + 1);
+          }
+        } else {
+          for (int i = a + 2 + g; i < T; i += NG - 1) {
+            upd_panel(i, a);
+            upd_panel(i, a + 1);
+          }
+        }
+        // (2)-(3) factor and solve the next panel
+        if (a < Tv) {
+          __syncwarp();
+          SPH(3);
+          g_factor_solve(a);
+          SPH(4);
+        }
+      }
+    } else if (in_u) {
+      // U: S_ij += L_i,c0 L_j,c0ᵀ (+ L_i,c1 L_j,c1ᵀ) for columns j ≥ a + 2, in row segments
+      // of up to SEG tiles (longest rows first; segment u → U-warp u mod NU), four tiles at
+      // a time (independent accumulators between a tile's DMMAs)
+      constexpr int SEG = 8;
+      const int j_lo = a + 2;
+      int uc = 0;
+      for (int i = T - 1; i >= j_lo; --i) {
+        const int nj = i - j_lo + 1;
+        const int nseg = (nj + SEG - 1) / SEG;
+        int u = uw - uc;
+        if (u < 0) u += ((-u + NU - 1) / NU) * NU;
+        for (; u < nseg; u += NU) {
+          const int j0 = j_lo + u * SEG, j1 = min(j0 + SEG - 1, i);
+          const double* L0 = tile(i, c0);
+          const double a00 = frag_ab(L0, lane, 0), a01 = frag_ab(L0, lane, 1);
+          double a10 = 0.0, a11 = 0.0;
+          if (two) {
+            const double* L1 = tile(i, c1);
+            a10 = frag_ab(L1, lane, 0);
+            a11 = frag_ab(L1, lane, 1);
+          }
+          for (int j = j0; j <= j1; j += 4) {
+            double bq[4][2], cq[4][2];
+            const int cnt = min(4, j1 - j + 1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q < cnt) {
+                const double* B0 = tile(j + q, c0);
+                bq[q][0] = frag_ab(B0, lane, 0);
+                bq[q][1] = frag_ab(B0, lane, 1);
+                const double2 cv = *reinterpret_cast<const double2*>(tile(i, j + q) + co);
+                cq[q][0] = cv.x;
+                cq[q][1] = cv.y;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < cnt) dmma8(cq[q], a00, bq[q][0]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < cnt) dmma8(cq[q], a01, bq[q][1]);
+            if (two) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (q < cnt) {
+                  const double* B1 = tile(j + q, c1);
+                  bq[q][0] = frag_ab(B1, lane, 0);
+                  bq[q][1] = frag_ab(B1, lane, 1);
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (q < cnt) dmma8(cq[q], a10, bq[q][0]);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (q < cnt) dmma8(cq[q], a11, bq[q][1]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q < cnt) *reinterpret_cast<double2*>(tile(i, j + q) + co) = make_double2(cq[q][0], cq[q][1]);
+          }
+        }
+        uc += nseg;
+      }
+    }
+    SPH(5);
     __syncthreads();
+    SPH(6);
   }
 
   if (flag[0]) {
@@ -284,9 +433,24 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
   }
   __syncthreads();
   point_epilogue(A, k, Cm, r, Q, A.p, logdet, flag, scal, tid, NT, LEAD * 32);
+  SPH(7);
+  SPH_FLUSH(LEAD, 0);
+  SPH_FLUSH(0, 1);
 }
 
 }  // namespace
+
+#ifdef LIK_PHASE_TIMERS
+extern "C" int lik_debug_small_phase_cycles(unsigned long long* out8, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_lik_small_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_lik_small_phase, z, sizeof z);
+  }
+  return 0;
+}
+#endif
 
 constexpr int SMALL_NMAX = 216;  // rows of the augmented matrix (n_pad + r_pad) the small path takes
 
@@ -323,14 +487,18 @@ cudaError_t launch_chol_small(const CholArgs& a, const double* coords, const dou
   const SmallLayout L = small_layout(a.g.n, a.g.r, a.p);
   const size_t smem = small_smem_bytes(L);
   cudaError_t e;
+#ifndef LIK_SMALL_NT
+#define LIK_SMALL_NT 512  // threads per SM (one CTA, or each of two CTAs with half)
+#endif
+  constexpr int NT1 = LIK_SMALL_NT, NT2 = LIK_SMALL_NT / 2;
   if (smem <= 113 * 1024) {  // two CTAs per SM: one's pivot chain beside the other's updates
-    e = cudaFuncSetAttribute(chol_small_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(chol_small_kernel<NT2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    chol_small_kernel<256><<<kw, 256, smem, st>>>(a, L, coords, Bt, ldb, table);
+    chol_small_kernel<NT2, 2><<<kw, NT2, smem, st>>>(a, L, coords, Bt, ldb, table);
   } else {
-    e = cudaFuncSetAttribute(chol_small_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(chol_small_kernel<NT1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    chol_small_kernel<512><<<kw, 512, smem, st>>>(a, L, coords, Bt, ldb, table);
+    chol_small_kernel<NT1, 1><<<kw, NT1, smem, st>>>(a, L, coords, Bt, ldb, table);
   }
   return cudaGetLastError();
 }
