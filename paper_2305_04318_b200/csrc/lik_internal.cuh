@@ -90,6 +90,9 @@ struct PointConst {
   int mode;                // MODE_*
   int e_zero;              // ρ ≡ 0 (ln ρ < −750) for s = z² ≥ 2^e_zero (set by table_kernel)
   int olo, ohi;            // table octaves built for this point (its range of s ± 1 octave)
+  int range_ok;            // the point's whole s range lies inside [2^(ELO+olo), 2^(ELO+ohi+1))
+                           // (not clipped at the table's ends): pairs of distinct sites need
+                           // no range check
 };
 
 // Per-point Chebyshev table of log2 ρ on binary octaves of s = z² = 8κ·d² ∈ [2^e,

@@ -101,6 +101,7 @@ __global__ void setup_kernel(const double* __restrict__ params, int K, PointCons
   P.e_zero = 1 << 20;  // set by table_kernel
   P.olo = 0;
   P.ohi = CHEB_NOCT - 1;
+  P.range_ok = 0;
   P.lnC = ok && P.mode == MODE_BESSEL ? matern_lnC(kappa) : 0.0;
   pc[k] = P;
 }
@@ -234,33 +235,15 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   const double s_lo = P.eightk * dstat[0] * q_lo, s_hi = P.eightk * dstat[1] * q_hi;
   const int olo = s_lo > 0.0 ? max(0, min(CHEB_NOCT - 1, ilogb(s_lo) - CHEB_ELO - 1)) : 0;
   const int ohi = s_hi > 0.0 ? max(olo, min(CHEB_NOCT - 1, ilogb(s_hi) - CHEB_ELO + 1)) : olo;
-  // interval edges: s = 2^(ELO + iv/SUB) · (1 + (iv mod SUB)/SUB)
-  for (int iv = olo * CHEB_SUB + tid; iv <= (ohi + 1) * CHEB_SUB; iv += 256)
-    edge[iv] = log_rho_exact(P, ldexp(1.0 + (double)(iv % CHEB_SUB) / CHEB_SUB, CHEB_ELO + iv / CHEB_SUB));
-  __syncthreads();
-  if (tid == 0) {
-    int e0 = CHEB_ELO + CHEB_NOCT + 64;  // sentinel: never underflows inside the table range
-    for (int o = olo; o <= ohi + 1; ++o)
-      if (edge[o * CHEB_SUB] < -750.0) {
-        e0 = CHEB_ELO + o;
-        break;
-      }
-    ez = e0;
-    pc[k].e_zero = e0;
-    pc[k].olo = olo;
-    pc[k].ohi = ohi;
-  }
-  __syncthreads();
-  // g = ln ρ(√s) − L_o(x) at the nodes, L_o the line through the interval's edge values
+  // ln ρ at the nodes (f, not yet detrended) and at the interval edges s = 2^(ELO + iv/SUB)
+  // · (1 + (iv mod SUB)/SUB) (edge), all from the octave's shared quadrature grid
   {
     const double kap = P.kappa, i4k = P.inv4k;
     double* qa = cheb + warp * 2 * QCAP;
     double* qb = qa + QCAP;
-    const bool active = lane < CHEB_SUB * CHEB_N;
-    const int part = active ? lane / CHEB_N : 0, i = active ? lane % CHEB_N : 0;
-    const double xc = cospi((i + 0.5) / CHEB_N);
-    const double lo = 1.0 + (double)part / CHEB_SUB, hw = 0.5 / CHEB_SUB;
-    for (int o = olo + warp; o <= ohi && CHEB_ELO + o < ez; o += 8) {
+    constexpr int NODES = CHEB_SUB * CHEB_N;
+    constexpr int NPASS = NODES + CHEB_SUB + 1 <= 32 ? 1 : 2;  // node lanes, then the edge lanes
+    for (int o = olo + warp; o <= ohi; o += 8) {
       const int e = CHEB_ELO + o;
       const double s0 = ldexp(1.0, e), s1 = 2.0 * s0;
       double x0, x1, h0, h;
@@ -282,32 +265,78 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
       }
       const double xl = x0 - L * h;
       const int nq = L + (int)ceil((x1 - x0) / h) + R + 1;
-      // this lane's node s and the peak of G(·; s) (the log-sum reference)
-      const double sn = ldexp(lo + hw * (1.0 + xc), e);
-      double xs, hs;
-      quad_peak_step(kap, sn, xs, hs);
-      const double gs = quad_G(kap, sn * i4k, xs);
-      double sum = 0.0;
-      for (int c0 = 0; c0 < nq; c0 += QCAP) {
-        __syncwarp();
-        for (int j = lane; j < QCAP && c0 + j < nq; j += 32) {
-          const double x = xl + (c0 + j) * h;
-          double ex, em;
-          quad_exp(x, ex, em);
-          qa[j] = kap * (x - em);
-          qb[j] = i4k / ex;
+      for (int pass = 0; pass < NPASS; ++pass) {
+        // this lane's s: a Chebyshev node (slot < NODES) or an interval edge
+        const int slot = NPASS == 1 ? lane : (pass == 0 ? lane : NODES + lane);
+        const bool is_node = slot < NODES;
+        const int eix = slot - NODES;  // edge index within the octave: 0..SUB (SUB = the top edge)
+        const bool active = is_node || (eix <= CHEB_SUB && (eix < CHEB_SUB || o == ohi));
+        double sn;
+        if (is_node) {
+          const int part = slot / CHEB_N, i = slot % CHEB_N;
+          sn = ldexp(1.0 + (double)part / CHEB_SUB + (0.5 / CHEB_SUB) * (1.0 + cospi((i + 0.5) / CHEB_N)), e);
+        } else {
+          sn = ldexp(1.0 + (double)min(eix, CHEB_SUB) / CHEB_SUB, e);
+        }
+        double xs, hs;
+        quad_peak_step(kap, sn, xs, hs);
+        const double gs = quad_G(kap, sn * i4k, xs);
+        double sum = 0.0;
+        for (int c0 = 0; c0 < nq; c0 += QCAP) {
+          __syncwarp();
+          for (int j = lane; j < QCAP && c0 + j < nq; j += 32) {  // (a second pass recomputes
+            const double x = xl + (c0 + j) * h;                   //  the grid chunk by chunk)
+            double ex, em;
+            quad_exp(x, ex, em);
+            qa[j] = kap * (x - em);
+            qb[j] = i4k / ex;
+          }
+          __syncwarp();
+          const int cn = min(QCAP, nq - c0);
+          if (active) {
+            // four partial sums (independent exp chains), combined in a fixed order
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            int j = 0;
+            for (; j + 4 <= cn; j += 4) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) s4[u] += exp(fma(-sn, qb[j + u], qa[j + u]) - gs);
+            }
+            for (; j < cn; ++j) s4[0] += exp(fma(-sn, qb[j], qa[j]) - gs);
+            sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          }
         }
         __syncwarp();
-        const int cn = min(QCAP, nq - c0);
-        for (int j = 0; j < cn; ++j) sum += exp(fma(-sn, qb[j], qa[j]) - gs);
-      }
-      __syncwarp();
-      if (active) {
-        const int iv = o * CHEB_SUB + part;
         const double lr = P.lnC + gs + log(h * sum);
-        f[iv * CHEB_N + i] = lr - 0.5 * (edge[iv] + edge[iv + 1]) - 0.5 * (edge[iv + 1] - edge[iv]) * xc;
+        if (is_node) {
+          const int part = slot / CHEB_N, i = slot % CHEB_N;
+          f[(o * CHEB_SUB + part) * CHEB_N + i] = lr;
+        } else if (active) {
+          edge[o * CHEB_SUB + eix] = lr;
+        }
       }
     }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int e0 = CHEB_ELO + CHEB_NOCT + 64;  // sentinel: never underflows inside the table range
+    for (int o = olo; o <= ohi + 1; ++o)
+      if (edge[o * CHEB_SUB] < -750.0) {
+        e0 = CHEB_ELO + o;
+        break;
+      }
+    ez = e0;
+    pc[k].e_zero = e0;
+    pc[k].olo = olo;
+    pc[k].ohi = ohi;
+    // a full octave of margin on both sides (neither end clipped at the table's limits)
+    pc[k].range_ok = s_lo >= ldexp(1.0, CHEB_ELO + olo + 1) && s_hi < ldexp(1.0, CHEB_ELO + ohi);
+  }
+  __syncthreads();
+  // detrend: g = ln ρ − L_iv(x), L_iv the line through the interval's edge values
+  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
+    const int iv = idx / CHEB_N, i = idx % CHEB_N;
+    const double xc = cospi((i + 0.5) / CHEB_N);
+    f[idx] -= 0.5 * (edge[iv] + edge[iv + 1]) + 0.5 * (edge[iv + 1] - edge[iv]) * xc;
   }
   __syncthreads();
   // Chebyshev coefficients of g (DCT-II), then monomial coefficients in t (T_j has
@@ -437,7 +466,10 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
           hx[e] = ri.x - cj.x;
           hy[e] = ri.y - cj.y;
         }
-        matern_rho_tableN<BUILD_NE, SUB>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+        if (regular && P.range_ok)
+          matern_rho_tableN<BUILD_NE, SUB, false>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+        else
+          matern_rho_tableN<BUILD_NE, SUB, true>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
 #pragma unroll
         for (int e = 0; e < BUILD_NE; ++e) Tc[(q + e) * 4 * KC] = v[e];
       }

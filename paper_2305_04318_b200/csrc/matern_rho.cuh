@@ -153,9 +153,11 @@ __device__ __forceinline__ double exp2_neg(double y, const double* etab) {
 // s = z² from the point's scaled rotation (no square root); the octave o of s is
 // clamped to [olo, oz] (oz: the underflow octave, or ohi); elements whose octave lies
 // outside [olo, ohs] (ohs = ohi, or "none" when the table reaches the underflow octave)
-// need the exact path and set bit `bit + e` of `slow` (s = 0 among them); their
-// returned value is meaningless.
-template <int NE, int SUB>
+// need the exact path and set bit `bit + e` of `slow`; their returned value is
+// meaningless.  CHECK = false skips the flags (five integer operations per element): for
+// the pairs of distinct real sites of a point whose s range lies inside its table
+// (PointConst::range_ok), which the table covers by construction.
+template <int NE, int SUB, bool CHECK = true>
 __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const double* coef,
                                                   const double* etab, int olo, int oz, unsigned span,
                                                   const double (&hx)[NE], const double (&hy)[NE],
@@ -170,13 +172,34 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
     const double sv = fma(u, u, w * w);  // s = z² = 8κ d²
     const int hi = __double2hiint(sv);
     const int o = (hi >> 20) - (1023 + CHEB_ELO);
-    slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
+    if (CHECK) slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
     const int oc = min(max(o, olo), oz);
     const int part = SUB == 1 ? 0 : (hi >> 19) & 1;
     const double scale = __hiloint2double((1023 + SUB - CHEB_ELO - oc) << 20, 0);
     t[e] = fma(sv, scale, SUB == 1 ? -3.0 : (part ? -7.0 : -5.0));
     cp[e] = reinterpret_cast<const double2*>(coef + (oc * SUB + part) * CHEB_STRIDE);
   }
+#ifdef LIK_BUILD_PREFETCH
+  // Horner with the next coefficient pair of every chain loaded one step ahead
+  double2 un[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) un[e] = cp[e][CHEB_N / 2 - 1];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double2 u = un[e];
+    un[e] = cp[e][CHEB_N / 2 - 2];
+    h[e] = fma(u.y, t[e], u.x);
+  }
+#pragma unroll
+  for (int mm = CHEB_N / 2 - 2; mm >= 0; --mm) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const double2 u = un[e];
+      if (mm > 0) un[e] = cp[e][mm - 1];
+      h[e] = fma(fma(h[e], t[e], u.y), t[e], u.x);
+    }
+  }
+#else
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const double2 u = cp[e][CHEB_N / 2 - 1];
@@ -190,6 +213,7 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
       h[e] = fma(fma(h[e], t[e], u.y), t[e], u.x);
     }
   }
+#endif
 #pragma unroll
   for (int e = 0; e < NE; ++e) v[e] = exp2_neg(h[e], etab);
 }

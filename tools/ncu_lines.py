@@ -1,9 +1,11 @@
-"""Top CUDA source lines of an ncu report by warp-stall samples (needs -lineinfo and
+"""Top CUDA source lines of an ncu report by warp-stall samples (or another per-instruction
+column, e.g. "Instructions Executed") (needs -lineinfo and
 --import-source on): the cuda,sass source page, SASS rows attributed to the preceding
-source line.  usage: python tools/ncu_lines.py REPORT [N]"""
+source line.  usage: python tools/ncu_lines.py REPORT [N] [COLUMN]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+METRIC = sys.argv[3] if len(sys.argv) > 3 else "Warp Stall Sampling (All Samples)"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -14,7 +16,7 @@ for r in rows:
         continue
     if r and r[0] == "Line No":
         hdr = {h: i for i, h in enumerate(r)}
-        ws = hdr["Warp Stall Sampling (All Samples)"]
+        ws = hdr[METRIC]
         continue
     if not hdr or len(r) <= ws:
         continue
