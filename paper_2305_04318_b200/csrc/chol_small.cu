@@ -68,10 +68,12 @@ __device__ __forceinline__ double frag_ab(const double* X, int lane, int kk) {
 
 // The lead warp: factor the 8×8 diagonal tile (stored as −A) and write −W = −L⁻¹ into
 // Wn and the pivots into piv; a pivot ≤ tol sets *bad.  Every lane holds the whole lower
-// triangle (36 doubles, broadcast loads) and factors it redundantly: no shuffles, so the
-// only serial chain is rsqrt → scale → update of the next pivot (≈ 90 cycles per pivot;
-// the one-row-per-lane version with shuffles took ≈ 2,200 cycles per tile).  Lane l < 8
-// then forms column l of W by forward substitution and stores it.
+// triangle (broadcast loads) and factors it redundantly: no shuffles, so the only serial
+// chain is rsqrt → scale → update of the next pivot (≈ 90 cycles per pivot; the
+// one-row-per-lane version with shuffles took ≈ 2,200 cycles per tile).  Lane l carries
+// column l of W = L⁻¹ along in axpy form (x ← e_l; after pivot m: x_m /= L_mm, x_i −=
+// L_im x_m), which consumes column m of L right after it is formed, so the registers of
+// the factored columns are free again.
 __device__ __forceinline__ void factor8(const double* Skk, double* Wn, double* piv, double tol,
                                         int* bad) {
   const int lane = threadIdx.x & 31, l = lane & 7;
@@ -81,30 +83,26 @@ __device__ __forceinline__ void factor8(const double* Skk, double* Wn, double* p
 #pragma unroll
     for (int j = 0; j <= i; ++j) a[i * (i + 1) / 2 + j] = -Skk[toff(i, j)];
   int fail = 0;
-  double rv[8], mypiv = 1.0;
+  double mypiv = 1.0;
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = (i == l) ? 1.0 : 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const double d = a[c * (c + 1) / 2 + c];
     fail |= !(d > tol);
     const double r = rsqrt(d);
-    rv[c] = r;
     if (l == c) mypiv = d;
-    a[c * (c + 1) / 2 + c] = d * r;
 #pragma unroll
-    for (int i = c + 1; i < 8; ++i) a[i * (i + 1) / 2 + c] *= r;
+    for (int i = c + 1; i < 8; ++i) a[i * (i + 1) / 2 + c] *= r;  // column c of L (below the diagonal)
 #pragma unroll
     for (int i = c + 1; i < 8; ++i)
 #pragma unroll
       for (int j = c + 1; j <= i; ++j) a[i * (i + 1) / 2 + j] -= a[i * (i + 1) / 2 + c] * a[j * (j + 1) / 2 + c];
-  }
-  // column l of W = L⁻¹: x_i = (δ_il − Σ_{m<i} L_im x_m) / L_ii
-  double x[8];
+    // W column l: x_c = x_c / L_cc, then x_i −= L_ic x_c
+    x[c] *= r;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double t = (i == l) ? 1.0 : 0.0;
-#pragma unroll
-    for (int m = 0; m < i; ++m) t -= a[i * (i + 1) / 2 + m] * x[m];
-    x[i] = t * rv[i];
+    for (int i = c + 1; i < 8; ++i) x[i] -= a[i * (i + 1) / 2 + c] * x[c];
   }
   if (lane < 8) {
 #pragma unroll
@@ -314,20 +312,73 @@ __global__ void __launch_bounds__(NT, MINB)
       // (1) columns a, a+1 (those < T) += panel (c0, c1), rows ≥ column; the lead takes
       // the diagonal block, the other G warps the rows ≥ a + 2
       if (a < T) {
-        auto upd_panel = [&](int i, int j) {
-          upd_tile(tile(i, j), tile(i, c0), tile(j, c0));
-          if (two) upd_tile(tile(i, j), tile(i, c1), tile(j, c1));
-        };
-        if (g == NG - 1) {
-          upd_panel(a, a);
-          if (a + 1 < T) {
-            upd_panel(a + 1, a);
-            upd_panel(a + 1, a + 1);
+        const int b = a + 1;  // < T when a < Tv; may be ≥ T only for a Schur column a
+        const int npc = two ? 2 : 1;
+        // fragments of the panel's rows a and b (the B operands of every update below)
+        double fa[2][2], fb[2][2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = q == 0 ? c0 : c1;
+          if (q < npc) {
+            fa[q][0] = frag_ab(tile(a, c), lane, 0);
+            fa[q][1] = frag_ab(tile(a, c), lane, 1);
+            if (b < T) {
+              fb[q][0] = frag_ab(tile(b, c), lane, 0);
+              fb[q][1] = frag_ab(tile(b, c), lane, 1);
+            }
           }
+        }
+        if (g == NG - 1) {
+          // the diagonal block (a, a), (b, a), (b, b): three independent accumulators
+          double acc[3][2];
+          const int nt3 = b < T ? 3 : 1;
+          double* C3[3] = {tile(a, a), b < T ? tile(b, a) : nullptr, b < T ? tile(b, b) : nullptr};
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+            if (t < nt3) {
+              const double2 cv = *reinterpret_cast<const double2*>(C3[t] + co);
+              acc[t][0] = cv.x;
+              acc[t][1] = cv.y;
+            }
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+              if (q < npc) {
+                dmma8(acc[0], fa[q][kk], fa[q][kk]);
+                if (nt3 == 3) {
+                  dmma8(acc[1], fb[q][kk], fa[q][kk]);
+                  dmma8(acc[2], fb[q][kk], fb[q][kk]);
+                }
+              }
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+            if (t < nt3) *reinterpret_cast<double2*>(C3[t] + co) = make_double2(acc[t][0], acc[t][1]);
         } else {
+          // rows i ≥ a + 2: tiles (i, a) and (i, b), two independent accumulators
           for (int i = a + 2 + g; i < T; i += NG - 1) {
-            upd_panel(i, a);
-            upd_panel(i, a + 1);
+            double acc[2][2];
+            double* Ca = tile(i, a);
+            double* Cb = tile(i, b);
+            double2 cv = *reinterpret_cast<const double2*>(Ca + co);
+            acc[0][0] = cv.x;
+            acc[0][1] = cv.y;
+            cv = *reinterpret_cast<const double2*>(Cb + co);
+            acc[1][0] = cv.x;
+            acc[1][1] = cv.y;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              if (q < npc) {
+                const double* Li = tile(i, q == 0 ? c0 : c1);
+                const double l0 = frag_ab(Li, lane, 0), l1 = frag_ab(Li, lane, 1);
+                dmma8(acc[0], l0, fa[q][0]);
+                dmma8(acc[1], l0, fb[q][0]);
+                dmma8(acc[0], l1, fa[q][1]);
+                dmma8(acc[1], l1, fb[q][1]);
+              }
+            }
+            *reinterpret_cast<double2*>(Ca + co) = make_double2(acc[0][0], acc[0][1]);
+            *reinterpret_cast<double2*>(Cb + co) = make_double2(acc[1][0], acc[1][1]);
           }
         }
         // (2)-(3) factor and solve the next panel
@@ -339,19 +390,24 @@ __global__ void __launch_bounds__(NT, MINB)
         }
       }
     } else if (in_u) {
-      // U: S_ij += L_i,c0 L_j,c0ᵀ (+ L_i,c1 L_j,c1ᵀ) for columns j ≥ a + 2, in row segments
-      // of up to SEG tiles (longest rows first; segment u → U-warp u mod NU), four tiles at
-      // a time (independent accumulators between a tile's DMMAs)
-      constexpr int SEG = 8;
+      // U: S_ij += L_i,c0 L_j,c0ᵀ (+ L_i,c1 L_j,c1ᵀ) for the tiles j_lo ≤ j ≤ i, j_lo = a + 2,
+      // taken row by row as one flat sequence split into NU equal contiguous ranges (balanced
+      // to ±1 tile); four tiles of a row at a time (independent accumulators between a
+      // tile's DMMAs, the row's L fragments reused)
       const int j_lo = a + 2;
-      int uc = 0;
-      for (int i = T - 1; i >= j_lo; --i) {
-        const int nj = i - j_lo + 1;
-        const int nseg = (nj + SEG - 1) / SEG;
-        int u = uw - uc;
-        if (u < 0) u += ((-u + NU - 1) / NU) * NU;
-        for (; u < nseg; u += NU) {
-          const int j0 = j_lo + u * SEG, j1 = min(j0 + SEG - 1, i);
+      const int mrows = T - j_lo;
+      if (mrows > 0) {
+        const int ntu = mrows * (mrows + 1) / 2;
+        int tau = (int)((long long)ntu * uw / NU);
+        const int tau_end = (int)((long long)ntu * (uw + 1) / NU);
+        // flat index → (i, j): row i = j_lo + ri holds ri + 1 tiles, starting at ri(ri+1)/2
+        int ri = (int)((sqrtf(8.0f * tau + 1.0f) - 1.0f) * 0.5f);
+        while ((ri + 1) * (ri + 2) / 2 <= tau) ++ri;
+        while (ri * (ri + 1) / 2 > tau) --ri;
+        int j = j_lo + (tau - ri * (ri + 1) / 2);
+        while (tau < tau_end) {
+          const int i = j_lo + ri;
+          const int cnt = min(min(4, i - j + 1), tau_end - tau);
           const double* L0 = tile(i, c0);
           const double a00 = frag_ab(L0, lane, 0), a01 = frag_ab(L0, lane, 1);
           double a10 = 0.0, a11 = 0.0;
@@ -360,48 +416,50 @@ __global__ void __launch_bounds__(NT, MINB)
             a10 = frag_ab(L1, lane, 0);
             a11 = frag_ab(L1, lane, 1);
           }
-          for (int j = j0; j <= j1; j += 4) {
-            double bq[4][2], cq[4][2];
-            const int cnt = min(4, j1 - j + 1);
+          double bq[4][2], cq[4][2];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < cnt) {
+              const double* B0 = tile(j + q, c0);
+              bq[q][0] = frag_ab(B0, lane, 0);
+              bq[q][1] = frag_ab(B0, lane, 1);
+              const double2 cv = *reinterpret_cast<const double2*>(tile(i, j + q) + co);
+              cq[q][0] = cv.x;
+              cq[q][1] = cv.y;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) dmma8(cq[q], a00, bq[q][0]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) dmma8(cq[q], a01, bq[q][1]);
+          if (two) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               if (q < cnt) {
-                const double* B0 = tile(j + q, c0);
-                bq[q][0] = frag_ab(B0, lane, 0);
-                bq[q][1] = frag_ab(B0, lane, 1);
-                const double2 cv = *reinterpret_cast<const double2*>(tile(i, j + q) + co);
-                cq[q][0] = cv.x;
-                cq[q][1] = cv.y;
+                const double* B1 = tile(j + q, c1);
+                bq[q][0] = frag_ab(B1, lane, 0);
+                bq[q][1] = frag_ab(B1, lane, 1);
               }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              if (q < cnt) dmma8(cq[q], a00, bq[q][0]);
+              if (q < cnt) dmma8(cq[q], a10, bq[q][0]);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              if (q < cnt) dmma8(cq[q], a01, bq[q][1]);
-            if (two) {
+              if (q < cnt) dmma8(cq[q], a11, bq[q][1]);
+          }
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (q < cnt) {
-                  const double* B1 = tile(j + q, c1);
-                  bq[q][0] = frag_ab(B1, lane, 0);
-                  bq[q][1] = frag_ab(B1, lane, 1);
-                }
-              }
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (q < cnt) dmma8(cq[q], a10, bq[q][0]);
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (q < cnt) dmma8(cq[q], a11, bq[q][1]);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (q < cnt) *reinterpret_cast<double2*>(tile(i, j + q) + co) = make_double2(cq[q][0], cq[q][1]);
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) *reinterpret_cast<double2*>(tile(i, j + q) + co) = make_double2(cq[q][0], cq[q][1]);
+          tau += cnt;
+          j += cnt;
+          if (j > i) {
+            ++ri;
+            j = j_lo;
           }
         }
-        uc += nseg;
       }
     }
     SPH(5);
@@ -487,10 +545,14 @@ cudaError_t launch_chol_small(const CholArgs& a, const double* coords, const dou
   const SmallLayout L = small_layout(a.g.n, a.g.r, a.p);
   const size_t smem = small_smem_bytes(L);
   cudaError_t e;
-#ifndef LIK_SMALL_NT
-#define LIK_SMALL_NT 512  // threads per SM (one CTA, or each of two CTAs with half)
+#ifndef LIK_SMALL_NT1
+#define LIK_SMALL_NT1 512  // threads of a CTA when one fits per SM
 #endif
-  constexpr int NT1 = LIK_SMALL_NT, NT2 = LIK_SMALL_NT / 2;
+#ifndef LIK_SMALL_NT2
+#define LIK_SMALL_NT2 256  // threads of each CTA when two fit per SM
+#endif
+  constexpr int NT1 = LIK_SMALL_NT1, NT2 = LIK_SMALL_NT2;
+  static_assert(NT1 >= 256 && NT2 >= 256, "the panel group takes four warps, the update group needs more");
   if (smem <= 113 * 1024) {  // two CTAs per SM: one's pivot chain beside the other's updates
     e = cudaFuncSetAttribute(chol_small_kernel<NT2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -219,9 +219,13 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   __shared__ double f[CHEB_NINT * CHEB_N];
   __shared__ double cheb[CHEB_NINT * CHEB_N];  // also the warps' quadrature scratch
   __shared__ double edge[CHEB_NINT + 1];
-  __shared__ int ez;
+  __shared__ int ez, next_oct;
+  __shared__ double etab[16];
+  constexpr double kLog2e = 1.4426950408889634074;
   __shared__ double tco[CHEB_N * CHEB_N];   // tco[j][k] = coefficient of t^k in T_j
   __shared__ double cosm[CHEB_N * CHEB_N];  // cosm[j][i] = cos(π j (i + ½) / N), the DCT-II matrix
+  if (tid < 16) etab[tid] = kExp2Tab[tid];
+  if (tid == 0) next_oct = 0;
   for (int e = tid; e < CHEB_N * CHEB_N; e += 256) {
     tco[e] = SUB == 1 ? kTco1.v[e] : kTco2.v[e];
     cosm[e] = cospi((e / CHEB_N) * ((e % CHEB_N) + 0.5) / CHEB_N);
@@ -235,6 +239,7 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   const double s_lo = P.eightk * dstat[0] * q_lo, s_hi = P.eightk * dstat[1] * q_hi;
   const int olo = s_lo > 0.0 ? max(0, min(CHEB_NOCT - 1, ilogb(s_lo) - CHEB_ELO - 1)) : 0;
   const int ohi = s_hi > 0.0 ? max(olo, min(CHEB_NOCT - 1, ilogb(s_hi) - CHEB_ELO + 1)) : olo;
+  __syncthreads();  // etab, next_oct
   // ln ρ at the nodes (f, not yet detrended) and at the interval edges s = 2^(ELO + iv/SUB)
   // · (1 + (iv mod SUB)/SUB) (edge), all from the octave's shared quadrature grid
   {
@@ -243,7 +248,13 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
     double* qb = qa + QCAP;
     constexpr int NODES = CHEB_SUB * CHEB_N;
     constexpr int NPASS = NODES + CHEB_SUB + 1 <= 32 ? 1 : 2;  // node lanes, then the edge lanes
-    for (int o = olo + warp; o <= ohi; o += 8) {
+    // octaves handed out dynamically (their grids differ a lot in length); each octave's
+    // values do not depend on which warp computes them
+    for (;;) {
+      int o = 0;
+      if (lane == 0) o = olo + atomicAdd(&next_oct, 1);
+      o = __shfl_sync(0xffffffffu, o, 0);
+      if (o > ohi) break;
       const int e = CHEB_ELO + o;
       const double s0 = ldexp(1.0, e), s1 = 2.0 * s0;
       double x0, x1, h0, h;
@@ -280,7 +291,7 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
         }
         double xs, hs;
         quad_peak_step(kap, sn, xs, hs);
-        const double gs = quad_G(kap, sn * i4k, xs);
+        const double gs = quad_G(kap, sn * i4k, xs), gs2 = kLog2e * gs;
         double sum = 0.0;
         for (int c0 = 0; c0 < nq; c0 += QCAP) {
           __syncwarp();
@@ -288,20 +299,21 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
             const double x = xl + (c0 + j) * h;                   //  the grid chunk by chunk)
             double ex, em;
             quad_exp(x, ex, em);
-            qa[j] = kap * (x - em);
-            qb[j] = i4k / ex;
+            qa[j] = kLog2e * (kap * (x - em));  // base 2: the terms are 2^(G·log2 e)
+            qb[j] = kLog2e * (i4k / ex);
           }
           __syncwarp();
           const int cn = min(QCAP, nq - c0);
           if (active) {
-            // four partial sums (independent exp chains), combined in a fixed order
+            // four partial sums (independent exp chains), combined in a fixed order; the
+            // table-driven 2^y (≤ 1 ulp; terms below 2^−1021 are 0, far below the e^−40 cut)
             double s4[4] = {0.0, 0.0, 0.0, 0.0};
             int j = 0;
             for (; j + 4 <= cn; j += 4) {
 #pragma unroll
-              for (int u = 0; u < 4; ++u) s4[u] += exp(fma(-sn, qb[j + u], qa[j + u]) - gs);
+              for (int u = 0; u < 4; ++u) s4[u] += exp2_neg(fma(-sn, qb[j + u], qa[j + u]) - gs2, etab);
             }
-            for (; j < cn; ++j) s4[0] += exp(fma(-sn, qb[j], qa[j]) - gs);
+            for (; j < cn; ++j) s4[0] += exp2_neg(fma(-sn, qb[j], qa[j]) - gs2, etab);
             sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
           }
         }
@@ -354,7 +366,6 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   // monomial coefficients of log2 ρ = log2(e)·(line + Σ c_j T_j(t)); the octave e_zero
   // (if built) holds the constant −2000, which the build's 2^y flushes to 0
   double* T = table + (size_t)blockIdx.x * TABLE_D;
-  constexpr double kLog2e = 1.4426950408889634074;
   for (int idx = olo * CHEB_SUB * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_STRIDE; idx += 256) {
     const int iv = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE;
     double a = 0.0;

@@ -4,6 +4,7 @@
 // not (neighbours on SMSP 3 or only on SMSPs 0-2).  Prints cycles per factor.
 #include <cstdio>
 #include <cuda_runtime.h>
+// v2 = 2: the lead times a chain of 64 dependent DMMAs (cycles per 64) instead
 
 __device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -104,7 +105,12 @@ __global__ void __launch_bounds__(512, 1) bench(int mode, int smsp3, int iters, 
   if (warp == lead) {
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
-      if (v2) factor8v2(S, W, piv, 1e-12, &bad); else factor8(S, W, piv, 1e-12, &bad);
+      if (v2 == 2) {
+        double c[2] = {S[lane], S[lane + 32]};
+#pragma unroll 1
+        for (int q = 0; q < 64; ++q) dmma8(c, 1.0000001, 0.5);
+        if (lane < 8) W[lane] = c[0] + c[1];
+      } else if (v2) factor8v2(S, W, piv, 1e-12, &bad); else factor8(S, W, piv, 1e-12, &bad);
       __syncwarp();
       if (lane < 8) S[toff(lane, lane)] = -10.0 - 1e-9 * it;  // keep a dependency
       __syncwarp();
@@ -139,7 +145,7 @@ int main() {
   cudaMalloc(&out, 148 * sizeof(long long));
   cudaMalloc(&sink, 148 * 512 * sizeof(double));
   const char* names[] = {"alone", "dmma", "lds/sts", "dfma"};
-  for (int v2 = 0; v2 < 2; ++v2)
+  for (int v2 = 0; v2 < 3; ++v2)
   for (int mode = 0; mode < 4; ++mode)
     for (int s3 = 0; s3 < 2; ++s3) {
       if (mode == 0 && s3) continue;
