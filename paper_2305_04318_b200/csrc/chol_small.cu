@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(NT, MINB)
     Cm[e] = S[tri8(Tv + hi / 8, Tv + lo / 8) * 64 + toff(hi & 7, lo & 7)];
   }
   __syncthreads();
-  point_epilogue(A, k, Cm, r, Q, A.p, logdet, flag, scal, tid, NT, LEAD * 32);
+  point_epilogue(A, k, Cm, r, Q, A.p, logdet, flag, scal, tid, NT, LEAD * 32, Q + A.p * A.p);
   SPH(7);
   SPH_FLUSH(LEAD, 0);
   SPH_FLUSH(0, 1);
@@ -522,8 +522,8 @@ static SmallLayout small_layout(int n, int r, int p) {
   L.off_tab = off;
   off += Cheb<1>::TABLE_D + 2 * n;  // table, then the sites
   L.off_sites = L.off_tab + Cheb<1>::TABLE_D;
-  // Cm (r×r) and Q (p×p) of the epilogue alias the table and the sites
-  off = std::max(off, L.off_tab + r * r + p * p);
+  // Cm (r×r), Q (p×p) and the c / β̂ rows of the epilogue alias the table and the sites
+  off = std::max(off, L.off_tab + r * r + p * p + 2 * r * p);  // + the epilogue's c, β̂ rows
   off = (off + 1) & ~1;
   L.off_w = off;
   off += 128;

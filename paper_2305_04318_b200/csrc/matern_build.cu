@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
       continue;
     }
     // tile (i, j) from the packed index
-    int i = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+    int i = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
     while (tri_index(i + 1, 0) <= tile) ++i;
     while (tri_index(i, 0) > tile) --i;
     const int j = tile - tri_index(i, 0);

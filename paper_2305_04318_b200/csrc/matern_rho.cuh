@@ -171,13 +171,20 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
     const double w = fma(P.qT, hx[e], P.qY * hy[e]);
     const double sv = fma(u, u, w * w);  // s = z² = 8κ d²
     const int hi = __double2hiint(sv);
-    const int o = (hi >> 20) - (1023 + CHEB_ELO);
-    if (CHECK) slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
-    const int oc = min(max(o, olo), oz);
+    if (CHECK) {
+      const int o = (hi >> 20) - (1023 + CHEB_ELO);
+      slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
+    }
+    // interval = SUB·octave + the top mantissa bit (SUB = 2): one shift of the high word;
+    // clamped to [SUB·olo, SUB·oz + SUB − 1] (above: the underflow octave's constant)
+    const int iv = min(max((hi >> (21 - SUB)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
+    // t ∈ [−1, 1) from the mantissa alone: 2^{SUB}·(1.mantissa) (exponent field set to
+    // 1023 + SUB) minus the interval's centre 2·SUB + 1 + 2·part — exact
+    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + SUB) << 20), __double2loint(sv));
     const int part = SUB == 1 ? 0 : (hi >> 19) & 1;
-    const double scale = __hiloint2double((1023 + SUB - CHEB_ELO - oc) << 20, 0);
-    t[e] = fma(sv, scale, SUB == 1 ? -3.0 : (part ? -7.0 : -5.0));
-    cp[e] = reinterpret_cast<const double2*>(coef + (oc * SUB + part) * CHEB_STRIDE);
+    const double centre = __hiloint2double((SUB == 1 ? 0x40080000 : 0x40140000) + (part << 19), 0);  // 3 | 5 or 7
+    t[e] = m4 - centre;
+    cp[e] = reinterpret_cast<const double2*>(coef + iv * CHEB_STRIDE);
   }
 #ifdef LIK_BUILD_PREFETCH
   // Horner with the next coefficient pair of every chain loaded one step ahead

@@ -35,12 +35,13 @@ __device__ inline void point_failure(const CholArgs& A, int k, int code, int tid
 // full), log|V| = logdet (valid in thread lead_tid): XᵀV⁻¹X = QQᵀ (Step 5, pivot ≤
 // p·ε·max diag ⇒ XVX_NOT_PD), c = Q⁻¹XᵀV⁻¹y' (Step 6), ssqBetahat = cᵀc (Step 7),
 // q = y'ᵀV⁻¹y' − ssqBetahat (Step 8; R12), β̂ = Q⁻ᵀc, σ̂² = q/n, ℓ_p, and the optional
-// Table-1 / REML outputs.  Q: p×p scratch (stride ldq); flag: ≥ 3 ints with flag[2] = 0
+// Table-1 / REML outputs.  Q: p×p scratch (stride ldq); scratch: NULL or 2·p·min(M, nthr)
+// doubles; flag: ≥ 3 ints with flag[2] = 0
 // on entry; scal: ≥ 3 doubles.  Called by all nthr threads of the CTA (it contains
 // barriers).
 __device__ inline void point_epilogue(const CholArgs& A, int k, const double* Cm, int ldc, double* Q,
                                       int ldq, double logdet, int* flag, double* scal, int tid,
-                                      int nthr, int lead_tid) {
+                                      int nthr, int lead_tid, double* scratch = nullptr) {
   const int M = A.M, p = A.p, r = M + p, n_sites = A.g.n;
   if (A.ssqYX)
     for (int e = tid; e < r * r; e += nthr) A.ssqYX[(size_t)k * r * r + e] = Cm[(e / r) * ldc + e % r];
@@ -82,7 +83,11 @@ __device__ inline void point_epilogue(const CholArgs& A, int k, const double* Cm
   const double ln2pi = 1.8378770664093454836;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   for (int m = tid; m < M; m += nthr) {
-    double cv[64], bt[64];
+    // c and β̂ of this λ: in `scratch` (shared memory, 2p doubles per thread) when given —
+    // local memory misses the small L1 left beside a large shared-memory carve-out
+    double cvl[64], btl[64];
+    double* cv = scratch ? scratch + 2 * p * tid : cvl;
+    double* bt = scratch ? cv + p : btl;
     double sb = 0.0;
     for (int a = 0; a < p; ++a) {  // Step 6: c = Q⁻¹ XᵀV⁻¹y'
       double s = Cm[(M + a) * ldc + m];
