@@ -29,7 +29,10 @@
  *     params: K×5 {φX, κ, ν², φR, φA [radians]}; lambdas: M.
  *   - outputs: loglik K×M (ℓ_p, not −2ℓ_p), betahat K×M×p, sigma2hat K×M,
  *     logdetV K, status K (LIK_PT_*).
- *   - limits: 1 ≤ p, n ≥ p + 2, K ≥ 1, M ≥ 1, M + p ≤ 64.
+ *   - limits: 1 ≤ p ≤ 63, n ≥ p + 2, K ≥ 1, M ≥ 1.  With M + p > 64 the λ are
+ *     evaluated in chunks of 64 − p (the factorisation is repeated per chunk; the
+ *     kernels take r = M + p ≤ 64); the Table-1 / REML outputs of
+ *     lik_eval_batch_device_ex and prepared datasets need M + p ≤ 64 (LIK_ENOTIMPL).
  *   - Call-level errors return < 0, write no outputs, and set the message
  *     returned by lik_last_error (naming the offending index).
  *   - Point-level failures never fail the call: status[k] != 0,
@@ -55,13 +58,13 @@ typedef struct lik_ctx lik_ctx; /* opaque */
 /* Call-level return codes. */
 enum {
   LIK_OK = 0,
-  LIK_EINVAL = -1,   /* NULL pointer, bad sizes (n < p+2, p < 1, K < 1, M < 1, M+p > 64),
+  LIK_EINVAL = -1,   /* NULL pointer, bad sizes (n < p+2, p < 1, p > 63, K < 1, M < 1),
                         non-finite coords / y / X / lambdas */
   LIK_EDOMAIN = -2,  /* some y_i <= 0 (Box-Cox needs log y) or two coincident sites */
   LIK_ERANK = -3,    /* X not of full column rank */
   LIK_ENOMEM = -4,   /* device workspace allocation failed */
   LIK_ECUDA = -5,    /* a CUDA runtime error (message has the CUDA error string) */
-  LIK_ENOTIMPL = -6  /* entry point or option not implemented */
+  LIK_ENOTIMPL = -6  /* entry point or option not implemented (summaries / datasets with M + p > 64) */
 };
 
 /* Per-point status codes (status[k]). */

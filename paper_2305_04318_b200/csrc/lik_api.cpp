@@ -46,6 +46,8 @@ struct lik_ctx {
   // host-API staging buffers
   char* io = nullptr;
   size_t io_bytes = 0;
+  char* chunk_buf = nullptr;  // per-chunk outputs when M + p > 64
+  size_t chunk_bytes = 0;
   int wave_points = 0;
   bool force_fused = std::getenv("LIK_NO_SMALL") != nullptr;  // A/B: keep chol_fused for small n
   // free-memory query of the last call (cudaMemGetInfo costs 0.1-5 ms of host time):
@@ -117,7 +119,7 @@ int validate(lik_ctx* c, int n, int p, const double* coords, const double* y, co
   if (n < p + 2) return fail(c, LIK_EINVAL, "n = %d < p + 2 = %d", n, p + 2);
   if (K < 1) return fail(c, LIK_EINVAL, "K = %d < 1", K);
   if (M < 1) return fail(c, LIK_EINVAL, "M = %d < 1", M);
-  if (M + p > 64) return fail(c, LIK_EINVAL, "M + p = %d > 64", M + p);
+  if (p > 63) return fail(c, LIK_EINVAL, "p = %d > 63", p);
   for (int i = 0; i < n; ++i)
     if (!std::isfinite(coords[2 * i]) || !std::isfinite(coords[2 * i + 1]))
       return fail(c, LIK_EINVAL, "coords[%d] is not finite", i);
@@ -420,6 +422,52 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   return LIK_OK;
 }
 
+// M + p > 64 (more λ than one augmented tile row holds): the λ are evaluated in chunks
+// of 64 − p, each a full pass (the factorisation is repeated per chunk — the kernels
+// keep r = M + p ≤ 64), into temporaries whose columns are copied into place; log|V| is
+// the same for every chunk; a point's status is the first failure, or NEG_RESID if any
+// chunk has a failed λ column.
+__global__ void merge_status_kernel(int K, const int* __restrict__ chunk, int* __restrict__ status) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int a = status[k], b = chunk[k];
+  if (a == LIK_PT_OK && b == LIK_PT_NEG_RESID) status[k] = LIK_PT_NEG_RESID;
+}
+
+int run_lambda_chunks(lik_ctx* c, int n, int p, const double* coords, const double* y, const double* X,
+                      int K, const double* params, int M, const double* lambdas, double* loglik,
+                      double* betahat, double* sigma2hat, double* logdetV, int* status,
+                      cudaStream_t st, const double* hcoords) {
+  const int Mc = 64 - p;
+  const size_t chunk_d = (size_t)K * Mc * (2 + p) + K;
+  int rc;
+  if ((rc = ensure(c, &c->chunk_buf, &c->chunk_bytes, chunk_d * 8 + (size_t)K * 4 + 64))) return rc;
+  double* cll = reinterpret_cast<double*>(c->chunk_buf);
+  double* cbh = cll + (size_t)K * Mc;
+  double* cs2 = cbh + (size_t)K * Mc * p;
+  double* cld = cs2 + (size_t)K * Mc;
+  int* cst = reinterpret_cast<int*>(cld + K);
+  for (int m0 = 0; m0 < M; m0 += Mc) {
+    const int mc = std::min(Mc, M - m0);
+    const bool first = m0 == 0;
+    if ((rc = run_device(c, n, p, coords, y, X, K, params, mc, lambdas + m0, cll, cbh, cs2,
+                         first ? logdetV : cld, first ? status : cst, st, hcoords)))
+      return rc;
+    CUDA_TRY(c, cudaMemcpy2DAsync(loglik + m0, (size_t)M * 8, cll, (size_t)mc * 8, (size_t)mc * 8, K,
+                                  cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaMemcpy2DAsync(sigma2hat + m0, (size_t)M * 8, cs2, (size_t)mc * 8, (size_t)mc * 8, K,
+                                  cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaMemcpy2DAsync(betahat + (size_t)m0 * p, (size_t)M * p * 8, cbh, (size_t)mc * p * 8,
+                                  (size_t)mc * p * 8, K, cudaMemcpyDeviceToDevice, st));
+    if (!first) {
+      merge_status_kernel<<<(K + 255) / 256, 256, 0, st>>>(K, cst, status);
+      CUDA_TRY(c, cudaGetLastError());
+    }
+    CUDA_TRY(c, mark_done(c, st));  // the chunk buffer is reused by the next chunk on st
+  }
+  return LIK_OK;
+}
+
 bool any_null(std::initializer_list<const void*> ps) {
   for (const void* q : ps)
     if (!q) return true;
@@ -468,6 +516,7 @@ void lik_destroy(lik_ctx* c) {
   cudaFree(c->perm);
   cudaFree(c->prof_scratch);
   cudaFree(c->io);
+  cudaFree(c->chunk_buf);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -495,8 +544,10 @@ int lik_eval_batch_device_ex(lik_ctx* c, int n, int p, const double* coords, con
   c->err.clear();
   if (any_null({coords, y, X, params, lambdas, loglik, betahat, sigma2hat, logdetV, status}))
     return fail(c, LIK_EINVAL, "NULL pointer argument");
-  if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || M + p > 64)
+  if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || p > 63)
     return validate(c, n, p, nullptr, nullptr, nullptr, K, M, nullptr);
+  if (M + p > 64 && (detReml || ssqYX || ssqBetahat || ssqResidual || loglik_reml || sigma2hat_reml))
+    return fail(c, LIK_ENOTIMPL, "the Table-1 / REML outputs need M + p <= 64 (M + p = %d)", M + p);
   HostTrace tr;
   CUDA_TRY(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -521,6 +572,9 @@ int lik_eval_batch_device_ex(lik_ctx* c, int n, int p, const double* coords, con
   ex.ssqResidual = ssqResidual;
   ex.loglik_reml = loglik_reml;
   ex.sigma2hat_reml = sigma2hat_reml;
+  if (M + p > 64)
+    return run_lambda_chunks(c, n, p, coords, y, X, K, params, M, lambdas, loglik, betahat,
+                             sigma2hat, logdetV, status, st, hc);
   return run_device(c, n, p, coords, y, X, K, params, M, lambdas, loglik, betahat, sigma2hat,
                     logdetV, status, st, hc, ex);
 }
@@ -533,7 +587,7 @@ int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double*
   c->err.clear();
   if (any_null({coords, y, X, params, lambdas, loglik, betahat, sigma2hat, logdetV, status}))
     return fail(c, LIK_EINVAL, "NULL pointer argument");
-  if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || M + p > 64)
+  if (n < 1 || p < 1 || M < 1 || K < 1 || n < p + 2 || p > 63)
     return validate(c, n, p, nullptr, nullptr, nullptr, K, M, nullptr);
   int rc = validate(c, n, p, coords, y, X, K, M, lambdas);
   if (rc) return rc;
@@ -559,7 +613,8 @@ int lik_eval_batch(lik_ctx* c, int n, int p, const double* coords, const double*
   CUDA_TRY(c, cudaMemcpyAsync(dX, X, (size_t)n * p * 8, cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(dp, params, (size_t)K * 5 * 8, cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(dl, lambdas, (size_t)M * 8, cudaMemcpyHostToDevice, st));
-  rc = run_device(c, n, p, dc, dy, dX, K, dp, M, dl, dll, dbh, ds2, dld, dst, st, coords);
+  rc = M + p > 64 ? run_lambda_chunks(c, n, p, dc, dy, dX, K, dp, M, dl, dll, dbh, ds2, dld, dst, st, coords)
+                  : run_device(c, n, p, dc, dy, dX, K, dp, M, dl, dll, dbh, ds2, dld, dst, st, coords);
   if (rc) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(loglik, dll, (size_t)K * M * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaMemcpyAsync(betahat, dbh, (size_t)K * M * p * 8, cudaMemcpyDeviceToHost, st));
@@ -625,6 +680,7 @@ int lik_dataset_create(lik_ctx* c, lik_dataset** out, int n, int p, const double
   if (any_null({coords, y, X, lambdas})) return fail(c, LIK_EINVAL, "NULL pointer argument");
   int rc = validate(c, n, p, coords, y, X, 1, M, lambdas);
   if (rc) return rc;
+  if (M + p > 64) return fail(c, LIK_ENOTIMPL, "a prepared dataset needs M + p <= 64 (M + p = %d)", M + p);
   CUDA_TRY(c, cudaSetDevice(c->device));
   const SlotGeom g = lik::make_geom(n, M + p);
   const int npad = g.nt * lik::TB;

@@ -247,11 +247,36 @@ def test_call_level_errors(ctx):
     assert rc == lik.LIK_ERANK
     rc, _ = ctx.eval_batch_rc(coords[:3], y[:3], X[:3], P, [0.5])
     assert rc == lik.LIK_EINVAL
-    rc, _ = ctx.eval_batch_rc(coords, y, X, P, np.linspace(0, 1, 63))
+    rc, _ = ctx.eval_batch_rc(coords, y, np.column_stack([X] * 32), P, [0.5])  # p = 64 > 63
     assert rc == lik.LIK_EINVAL
     c4 = coords.copy()
     c4[3, 0] = float("nan")
     assert ctx.eval_batch_rc(c4, y, X, P, [0.5])[0] == lik.LIK_EINVAL
+
+
+def test_many_lambdas_in_chunks(ctx, orc):
+    """M + p > 64: the λ are evaluated in chunks of 64 − p (one factorisation per chunk)
+    and copied into place — vs the oracle, and each chunk's columns bitwise equal to a
+    call with just that chunk's λ; the summaries and prepared datasets refuse it."""
+    coords, y, X = synthgen.make_dataset("C1")
+    p = X.shape[1]
+    lam = np.linspace(-1.0, 2.0, 150)  # 3 chunks of 62 (p = 2)
+    P = np.array([[900.0, 1.5, 0.2, 1.0, 0.0], [600.0, 0.7, 0.4, 1.0, 0.0], [-1.0, 1.5, 0.2, 1.0, 0.0]])
+    gpu = ctx.eval_batch(coords, y, X, P, lam)
+    assert_parity(gpu, _oracle(orc, coords, y, X, P, lam), label="chunks")
+    Mc = 64 - p
+    for m0 in range(0, len(lam), Mc):
+        part = ctx.eval_batch(coords, y, X, P, lam[m0:m0 + Mc])
+        for key in ("loglik", "sigma2hat", "betahat"):
+            assert np.array_equal(gpu[key][:, m0:m0 + Mc], part[key], equal_nan=True), (m0, key)
+        assert np.array_equal(gpu["logdetV"], part["logdetV"], equal_nan=True)
+    t = [torch.tensor(a, device="cuda") for a in (coords, y, X, P, lam)]
+    with pytest.raises(lik.LikError) as e:
+        ctx.eval_batch_device_ex(*t)
+    assert e.value.code == lik.LIK_ENOTIMPL
+    with pytest.raises(lik.LikError) as e:
+        ctx.dataset(coords, y, X, lam)
+    assert e.value.code == lik.LIK_ENOTIMPL
 
 
 def test_wide_r_and_gaussian_limit(ctx, orc):
