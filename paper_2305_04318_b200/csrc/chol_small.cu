@@ -115,7 +115,8 @@ __device__ __forceinline__ void factor8(const double* Skk, double* Wn, double* p
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     chol_small_kernel(CholArgs A, SmallLayout Lt, const double* __restrict__ coords,
-                      const double* __restrict__ Bt, int ldb, const double* __restrict__ table) {
+                      const double* __restrict__ Bt, int ldb, const double* __restrict__ table,
+                      cudaTextureObject_t table_tex) {
   constexpr int NW = NT / 32, LEAD = NW - 1;
   constexpr int CHEB_STRIDE = Cheb<1>::STRIDE;
   extern __shared__ __align__(16) double sm[];
@@ -190,7 +191,13 @@ __global__ void __launch_bounds__(NT, MINB)
     if (vtile) {
 #endif
       if (P.mode == MODE_BESSEL) {
+#if LIK_BUILD_TEXMASK
+        // some coefficient pairs through the texture path (see matern_rho.cuh)
+        matern_rho_tableN_tex<4, 1>(P, table_tex, (long long)blockIdx.x * (Cheb<1>::TABLE_D / 2), coef, etab,
+                                    olo, oz, span, hx, hy, rho, slow, 0);
+#else
         matern_rho_tableN<4, 1>(P, coef, etab, olo, oz, span, hx, hy, rho, slow, 0);
+#endif
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e) rho[e] = exp(-2.0 * aniso_d2(P, hx[e], hy[e]));
@@ -541,7 +548,7 @@ bool small_path_fits(int n, int r, int p) {
 }
 
 cudaError_t launch_chol_small(const CholArgs& a, const double* coords, const double* Bt, int ldb,
-                              const double* table, int kw, cudaStream_t st) {
+                              const double* table, cudaTextureObject_t table_tex, int kw, cudaStream_t st) {
   const SmallLayout L = small_layout(a.g.n, a.g.r, a.p);
   const size_t smem = small_smem_bytes(L);
   cudaError_t e;
@@ -556,11 +563,11 @@ cudaError_t launch_chol_small(const CholArgs& a, const double* coords, const dou
   if (smem <= 113 * 1024) {  // two CTAs per SM: one's pivot chain beside the other's updates
     e = cudaFuncSetAttribute(chol_small_kernel<NT2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    chol_small_kernel<NT2, 2><<<kw, NT2, smem, st>>>(a, L, coords, Bt, ldb, table);
+    chol_small_kernel<NT2, 2><<<kw, NT2, smem, st>>>(a, L, coords, Bt, ldb, table, table_tex);
   } else {
     e = cudaFuncSetAttribute(chol_small_kernel<NT1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    chol_small_kernel<NT1, 1><<<kw, NT1, smem, st>>>(a, L, coords, Bt, ldb, table);
+    chol_small_kernel<NT1, 1><<<kw, NT1, smem, st>>>(a, L, coords, Bt, ldb, table, table_tex);
   }
   return cudaGetLastError();
 }

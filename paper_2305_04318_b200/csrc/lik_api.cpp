@@ -36,6 +36,9 @@ struct lik_ctx {
   double* S = nullptr;
   double* table = nullptr;
   size_t table_bytes = 0;
+  cudaTextureObject_t table_tex = 0;  // over `table` (the build's texture-path coefficient loads)
+  const double* table_tex_ptr = nullptr;
+  size_t table_tex_bytes = 0;
   double* coords_p = nullptr;  // sites in Morton order (device)
   size_t coords_p_bytes = 0;
   int* perm = nullptr;         // Morton order (device)
@@ -209,6 +212,24 @@ struct HostTrace {
   }
 };
 
+// The texture object over the table buffer (re-created when the buffer changes).
+int table_texture(lik_ctx* c) {
+  if (c->table_tex && c->table_tex_ptr == c->table && c->table_tex_bytes == c->table_bytes) return LIK_OK;
+  if (c->table_tex) cudaDestroyTextureObject(c->table_tex);
+  c->table_tex = 0;
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = c->table;
+  rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+  rd.res.linear.sizeInBytes = c->table_bytes / 16 * 16;
+  cudaTextureDesc td = {};
+  td.readMode = cudaReadModeElementType;
+  CUDA_TRY(c, cudaCreateTextureObject(&c->table_tex, &rd, &td, nullptr));
+  c->table_tex_ptr = c->table;
+  c->table_tex_bytes = c->table_bytes;
+  return LIK_OK;
+}
+
 // Order this call's work on `st` after the previous call's (any stream).
 cudaError_t after_previous(lik_ctx* c, cudaStream_t st) {
   return c->done_recorded ? cudaStreamWaitEvent(st, c->done_ev, 0) : cudaSuccess;
@@ -324,6 +345,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
   c->pc_cap = pcb / sizeof(PointConst);
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)W * lik::TABLE_D * sizeof(double))))
     return rc;
+  if ((rc = table_texture(c))) return rc;
   const bool timing = c->flags & LIK_FLAG_TIMING;
   const int nwaves = (K + W - 1) / W;
   size_t ei = 0;
@@ -369,7 +391,8 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
       Nvtx nvb("lik.build");
       CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, k0, kw, c->table, S + 1, st));
       if (!small)
-        CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table, bt, c->ws, st));
+        CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords_p, g, c->pc, k0, kw, c->table,
+                                      c->table_tex, bt, c->ws, st));
     }
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
     lik::CholArgs a;
@@ -394,7 +417,7 @@ int run_device(lik_ctx* c, int n, int p, const double* coords, const double* y, 
     a.sigma2hat_reml = ex.sigma2hat_reml;
     Nvtx nvc("lik.chol");
     if (small)
-      CUDA_TRY(c, lik::launch_chol_small(a, coords_p, bt, g.nt * lik::TB, c->table, kw, st));
+      CUDA_TRY(c, lik::launch_chol_small(a, coords_p, bt, g.nt * lik::TB, c->table, c->table_tex, kw, st));
     else
       CUDA_TRY(c, lik::launch_chol(a, kw, st));
     if (timing) CUDA_TRY(c, cudaEventRecord(ev_get(c, ei++), st));
@@ -519,6 +542,7 @@ void lik_destroy(lik_ctx* c) {
   cudaFree(c->chunk_buf);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
+  if (c->table_tex) cudaDestroyTextureObject(c->table_tex);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -790,12 +814,14 @@ int lik_debug_build_V(lik_ctx* c, int n, const double* coords, int K, const doub
   c->pc_cap = pcb / sizeof(PointConst);
   if ((rc = ensure(c, &c->table, &c->table_bytes, (size_t)K * lik::TABLE_D * sizeof(double))))
     return rc;
+  if ((rc = table_texture(c))) return rc;
   if (!c->S) CUDA_TRY(c, cudaMalloc(&c->S, 4 * sizeof(double)));
   CUDA_TRY(c, after_previous(c, st));
   CUDA_TRY(c, lik::launch_dist_range(coords, n, c->S + 1, st));
   CUDA_TRY(c, lik::launch_setup(params, K, c->pc, st));
   CUDA_TRY(c, lik::launch_table(lik::cheb_sub_for(g.n), c->pc, 0, K, c->table, c->S + 1, st));
-  CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords, g, c->pc, 0, K, c->table, nullptr, c->ws, st));
+  CUDA_TRY(c, lik::launch_build(lik::cheb_sub_for(g.n), coords, g, c->pc, 0, K, c->table, c->table_tex,
+                                nullptr, c->ws, st));
   CUDA_TRY(c, lik::launch_unpack_V(g, c->pc, K, c->ws, V, st));
   CUDA_TRY(c, mark_done(c, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));

@@ -141,9 +141,14 @@ cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream
 cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st);
 cudaError_t launch_table(int sub, PointConst* pc, int k0, int kw, double* table, const double* dstat,
                          cudaStream_t st);
+#ifndef LIK_BUILD_TEXMASK
+#define LIK_BUILD_TEXMASK 0x24  // coefficient pairs fetched through the texture path (0: none)
+#endif
+// table_tex: a texture object (int4 elements) over `table` for the build's texture-path
+// coefficient loads (make_table_tex)
 cudaError_t launch_build(int sub, const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
-                         int kw, const double* table, const double* Bt, double* ws,
-                         cudaStream_t st);
+                         int kw, const double* table, cudaTextureObject_t table_tex, const double* Bt,
+                         double* ws, cudaStream_t st);
 cudaError_t launch_unpack_V(const SlotGeom& g, const PointConst* pc, int kw, const double* ws,
                             double* V, cudaStream_t st);
 
@@ -173,7 +178,7 @@ cudaError_t launch_chol(const CholArgs& a, int kw, cudaStream_t st);
 // workspace); small_path_fits says whether (n, r = M + p) takes it.
 bool small_path_fits(int n, int r, int p);
 cudaError_t launch_chol_small(const CholArgs& a, const double* coords, const double* Bt, int ldb,
-                              const double* table, int kw, cudaStream_t st);
+                              const double* table, cudaTextureObject_t table_tex, int kw, cudaStream_t st);
 size_t chol_smem_bytes();
 int profile_slices(long long K, int M);                       // slices of the (k, m) range
 size_t profile_partials(int p, int G, int Sg, int M, int nsl);  // doubles of partial maxima

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
                                                     const PointConst* __restrict__ pc, int k0,
                                                     const double* __restrict__ table,
                                                     const double* __restrict__ Bt,
-                                                    double* __restrict__ ws) {
+                                                    double* __restrict__ ws, cudaTextureObject_t tex) {
   constexpr int CHEB_STRIDE = Cheb<SUB>::STRIDE, TABLE_D = Cheb<SUB>::TABLE_D;
   const int slot = blockIdx.y;
   const PointConst P = pc[k0 + slot];
@@ -477,10 +477,18 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
           hx[e] = ri.x - cj.x;
           hy[e] = ri.y - cj.y;
         }
+#if LIK_BUILD_TEXMASK
+        const long long tb = (long long)slot * (TABLE_D / 2);
+        if (regular && P.range_ok)
+          matern_rho_tableN_tex<BUILD_NE, SUB, false>(P, tex, tb, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+        else
+          matern_rho_tableN_tex<BUILD_NE, SUB, true>(P, tex, tb, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+#else
         if (regular && P.range_ok)
           matern_rho_tableN<BUILD_NE, SUB, false>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
         else
           matern_rho_tableN<BUILD_NE, SUB, true>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+#endif
 #pragma unroll
         for (int e = 0; e < BUILD_NE; ++e) Tc[(q + e) * 4 * KC] = v[e];
       }
@@ -517,13 +525,14 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
 }
 
 cudaError_t launch_build(int sub, const double* coords, const SlotGeom& g, const PointConst* pc, int k0,
-                         int kw, const double* table, const double* Bt, double* ws,
-                         cudaStream_t st) {
+                         int kw, const double* table, cudaTextureObject_t table_tex, const double* Bt,
+                         double* ws, cudaStream_t st) {
+  const cudaTextureObject_t tex = table_tex;
   dim3 grid((g.ntri + g.nt + BUILD_TILES - 1) / BUILD_TILES, kw);
   if (sub == 2)
-    build_kernel<2><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
+    build_kernel<2><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
   else
-    build_kernel<1><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws);
+    build_kernel<1><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
   return cudaGetLastError();
 }
 

@@ -225,4 +225,66 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
   for (int e = 0; e < NE; ++e) v[e] = exp2_neg(h[e], etab);
 }
 
+#if LIK_BUILD_TEXMASK
+// The build's coefficient loads split between two pipes: the pairs mm with bit mm of
+// LIK_BUILD_TEXMASK set come through the texture path (tex1Dfetch<int4> on the table in
+// global memory, L1-resident), the others from shared memory.  With every pair from
+// shared memory the build was bound by the shared-memory data pipe (88 % of its
+// wavefronts, ~2.2 distinct intervals per quarter-warp: each LDS.128 took 4 wavefronts);
+// all through the texture path: 325 ms per C4 step; two of the eight pairs (mm 2 and 5):
+// 165 ms (from 194), DESIGN.md §5.
+template <int NE, int SUB, bool CHECK = true>
+__device__ __forceinline__ void matern_rho_tableN_tex(const PointConst& P, cudaTextureObject_t tex,
+                                                      long long tbase, const double* coef,
+                                                      const double* etab, int olo,
+                                                      int oz, unsigned span, const double (&hx)[NE],
+                                                      const double (&hy)[NE], double (&v)[NE],
+                                                      unsigned& slow, int bit) {
+  constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
+  double t[NE], h[NE];
+  long long cp[NE];
+  int ci[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double u = fma(P.qX, hx[e], -P.qS * hy[e]);
+    const double w = fma(P.qT, hx[e], P.qY * hy[e]);
+    const double sv = fma(u, u, w * w);
+    const int hi = __double2hiint(sv);
+    if (CHECK) {
+      const int o = (hi >> 20) - (1023 + CHEB_ELO);
+      slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
+    }
+    const int iv = min(max((hi >> (21 - SUB)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
+    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + SUB) << 20), __double2loint(sv));
+    const int part = SUB == 1 ? 0 : (hi >> 19) & 1;
+    const double centre = __hiloint2double((SUB == 1 ? 0x40080000 : 0x40140000) + (part << 19), 0);
+    t[e] = m4 - centre;
+    cp[e] = tbase + (long long)iv * (CHEB_STRIDE / 2);
+    ci[e] = iv * CHEB_STRIDE;
+  }
+  auto fetch = [&](int e, int mm) {
+    if ((LIK_BUILD_TEXMASK >> mm) & 1) {
+      const int4 q = tex1Dfetch<int4>(tex, (int)(cp[e] + mm));
+      return make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
+    }
+    return reinterpret_cast<const double2*>(coef + ci[e])[mm];
+  };
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double2 u = fetch(e, CHEB_N / 2 - 1);
+    h[e] = fma(u.y, t[e], u.x);
+  }
+#pragma unroll
+  for (int mm = CHEB_N / 2 - 2; mm >= 0; --mm) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const double2 u = fetch(e, mm);
+      h[e] = fma(fma(h[e], t[e], u.y), t[e], u.x);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) v[e] = exp2_neg(h[e], etab);
+}
+#endif
+
 }  // namespace lik
