@@ -30,14 +30,26 @@
 #include "point_epilogue.cuh"
 
 #ifdef LIK_PHASE_TIMERS
-__device__ unsigned long long g_lik_small_phase[16];
-#define SPH_INIT() long long sph_t = clock64(); long long sph_acc[8] = {0}
-#define SPH(i) do { const long long t_ = clock64(); sph_acc[i] += t_ - sph_t; sph_t = t_; } while (0)
-#define SPH_FLUSH(w, slot) do { if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) == (w)) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_lik_small_phase[8 * (slot) + i_], (unsigned long long)sph_acc[i_]); } while (0)
+__device__ unsigned long long g_lik_small_phase[36];
+// (the clock read carries a memory clobber so it stays on its side of the barriers; a
+// BAR.SYNC still blocks the warp only at a later instruction, so a barrier's wait can show
+// up in the phase after it)
+__device__ __forceinline__ long long sph_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : : "memory");
+  return t;
+}
+#define SPH_INIT() long long sph_t = sph_clock(); long long sph_acc[12] = {0}
+#define SPH(i) do { const long long t_ = sph_clock(); sph_acc[i] += t_ - sph_t; sph_t = t_; } while (0)
+#define SPH_FLUSH(w, slot) do { if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) == (w)) for (int i_ = 0; i_ < 12; ++i_) atomicAdd(&g_lik_small_phase[12 * (slot) + i_], (unsigned long long)sph_acc[i_]); } while (0)
 #else
 #define SPH_INIT() do {} while (0)
 #define SPH(i) do {} while (0)
 #define SPH_FLUSH(w, slot) do {} while (0)
+#endif
+
+#ifndef LIK_SMALL_UCH
+#define LIK_SMALL_UCH 3  // trailing-update tiles per chunk (independent accumulators; 3: C2 −3 %, Swiss −2 % vs 4)
 #endif
 
 namespace lik {
@@ -297,7 +309,9 @@ __global__ void __launch_bounds__(NT, MINB)
         factor8(tile(b, b), Wb, dlog + 8 * b, tol, &flag[0]);
       }
     }
+    SPH(8);
     g_bar();
+    SPH(9);
     if (g < NG - 1) {
       for (int i = a + 2 + g; i < T; i += NG - 1) {
         solve_tile(tile(i, a), Wa);
@@ -399,8 +413,9 @@ __global__ void __launch_bounds__(NT, MINB)
     } else if (in_u) {
       // U: S_ij += L_i,c0 L_j,c0ᵀ (+ L_i,c1 L_j,c1ᵀ) for the tiles j_lo ≤ j ≤ i, j_lo = a + 2,
       // taken row by row as one flat sequence split into NU equal contiguous ranges (balanced
-      // to ±1 tile); four tiles of a row at a time (independent accumulators between a
+      // to ±1 tile); UCH tiles of a row at a time (independent accumulators between a
       // tile's DMMAs, the row's L fragments reused)
+      constexpr int UCH = LIK_SMALL_UCH;
       const int j_lo = a + 2;
       const int mrows = T - j_lo;
       if (mrows > 0) {
@@ -414,7 +429,7 @@ __global__ void __launch_bounds__(NT, MINB)
         int j = j_lo + (tau - ri * (ri + 1) / 2);
         while (tau < tau_end) {
           const int i = j_lo + ri;
-          const int cnt = min(min(4, i - j + 1), tau_end - tau);
+          const int cnt = min(min(UCH, i - j + 1), tau_end - tau);
           const double* L0 = tile(i, c0);
           const double a00 = frag_ab(L0, lane, 0), a01 = frag_ab(L0, lane, 1);
           double a10 = 0.0, a11 = 0.0;
@@ -423,9 +438,9 @@ __global__ void __launch_bounds__(NT, MINB)
             a10 = frag_ab(L1, lane, 0);
             a11 = frag_ab(L1, lane, 1);
           }
-          double bq[4][2], cq[4][2];
+          double bq[UCH][2], cq[UCH][2];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < UCH; ++q) {
             if (q < cnt) {
               const double* B0 = tile(j + q, c0);
               bq[q][0] = frag_ab(B0, lane, 0);
@@ -436,14 +451,16 @@ __global__ void __launch_bounds__(NT, MINB)
             }
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < UCH; ++q)
             if (q < cnt) dmma8(cq[q], a00, bq[q][0]);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < UCH; ++q)
             if (q < cnt) dmma8(cq[q], a01, bq[q][1]);
           if (two) {
+            // (the second column's fragments loaded after the first column's DMMAs: loading
+            // them up front costs registers, and the spills cost more than the latency)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < UCH; ++q) {
               if (q < cnt) {
                 const double* B1 = tile(j + q, c1);
                 bq[q][0] = frag_ab(B1, lane, 0);
@@ -451,14 +468,14 @@ __global__ void __launch_bounds__(NT, MINB)
               }
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < UCH; ++q)
               if (q < cnt) dmma8(cq[q], a10, bq[q][0]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < UCH; ++q)
               if (q < cnt) dmma8(cq[q], a11, bq[q][1]);
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < UCH; ++q)
             if (q < cnt) *reinterpret_cast<double2*>(tile(i, j + q) + co) = make_double2(cq[q][0], cq[q][1]);
           tau += cnt;
           j += cnt;
@@ -501,16 +518,17 @@ __global__ void __launch_bounds__(NT, MINB)
   SPH(7);
   SPH_FLUSH(LEAD, 0);
   SPH_FLUSH(0, 1);
+  SPH_FLUSH(NW - 4, 2);
 }
 
 }  // namespace
 
 #ifdef LIK_PHASE_TIMERS
-extern "C" int lik_debug_small_phase_cycles(unsigned long long* out8, int reset) {
+extern "C" int lik_debug_small_phase_cycles(unsigned long long* out36, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out8, g_lik_small_phase, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out36, g_lik_small_phase, sizeof(unsigned long long) * 36);
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[36] = {0};
     cudaMemcpyToSymbol(g_lik_small_phase, z, sizeof z);
   }
   return 0;

@@ -522,6 +522,13 @@ int lik_create(lik_ctx** out, int cuda_device, unsigned flags) {
     delete c;
     return LIK_ECUDA;
   }
+  // the table kernel's DCT matrices (device globals of this device; idempotent)
+  if (lik::launch_cheb_init(c->own_stream) != cudaSuccess || cudaStreamSynchronize(c->own_stream) != cudaSuccess) {
+    cudaEventDestroy(c->done_ev);
+    cudaStreamDestroy(c->own_stream);
+    delete c;
+    return LIK_ECUDA;
+  }
   *out = c;
   return LIK_OK;
 }

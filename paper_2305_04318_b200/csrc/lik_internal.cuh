@@ -136,6 +136,8 @@ cudaError_t launch_prep(const double* coords, const double* y, const double* X,
                         const double* lambdas, const int* perm, int n, int p, int M, int npad,
                         double* coords_p, double* Bt, double* S, cudaStream_t st);
 cudaError_t launch_setup(const double* params, int K, PointConst* pc, cudaStream_t st);
+// once per process (lik_create): the DCT matrices of the table kernel
+cudaError_t launch_cheb_init(cudaStream_t st);
 // dist_range: dstat[0] = min, dstat[1] = max squared Euclidean distance over the
 // site pairs (bounds each point's range of s = z² for the table).
 cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st);

@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(256) dist_range_kernel(const double* __restric
 cudaError_t launch_dist_range(const double* coords, int n, double* dstat, cudaStream_t st) {
   dist_init_kernel<<<1, 1, 0, st>>>(dstat);
   const long long np = (long long)n * (n - 1) / 2;
-  const int blocks = (int)std::max<long long>(1, std::min<long long>(1184, (np + 256 * 64 - 1) / (256 * 64)));
+  // ~4 pairs per thread (a latency chain each: the pair index needs a square root)
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(1184, (np + 256 * 4 - 1) / (256 * 4)));
   dist_range_kernel<<<blocks, 256, 0, st>>>(coords, n, dstat);
   return cudaGetLastError();
 }
@@ -177,6 +178,20 @@ constexpr TcoTable<N> make_tco() {
     for (int kk = 0; kk < N; ++kk)
       t.v[jj * N + kk] = (kk > 0 ? 2.0 * t.v[(jj - 1) * N + kk - 1] : 0.0) - t.v[(jj - 2) * N + kk];
   return t;
+}
+// The DCT-II matrices cos(π j (i + ½) / N) of both layouts, written once per process by
+// cheb_init_kernel (lik_create) instead of 400 cospi per point in every table block.
+__device__ double g_cosm1[Cheb<1>::N * Cheb<1>::N];
+__device__ double g_cosm2[Cheb<2>::N * Cheb<2>::N];
+__global__ void cheb_init_kernel() {
+  for (int e = threadIdx.x; e < Cheb<1>::N * Cheb<1>::N; e += blockDim.x)
+    g_cosm1[e] = cospi((e / Cheb<1>::N) * ((e % Cheb<1>::N) + 0.5) / Cheb<1>::N);
+  for (int e = threadIdx.x; e < Cheb<2>::N * Cheb<2>::N; e += blockDim.x)
+    g_cosm2[e] = cospi((e / Cheb<2>::N) * ((e % Cheb<2>::N) + 0.5) / Cheb<2>::N);
+}
+cudaError_t launch_cheb_init(cudaStream_t st) {
+  cheb_init_kernel<<<1, 256, 0, st>>>();
+  return cudaGetLastError();
 }
 __device__ const TcoTable<Cheb<1>::N> kTco1 = make_tco<Cheb<1>::N>();
 __device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
@@ -203,15 +218,19 @@ __device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
 // G(x; s) = A − s·B costs one FMA and its term one exp.
 // ---------------------------------------------------------------------------
 constexpr int QCAP = 64;  // grid nodes per warp chunk
+#ifndef LIK_TABLE_NT
+#define LIK_TABLE_NT 256  // threads per point (the octaves are spread over its warps)
+#endif
+constexpr int TABLE_NT = LIK_TABLE_NT;
 
 template <int SUB>
-__global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc, int k0,
+__global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict__ pc, int k0,
                                                     double* __restrict__ table,
                                                     const double* __restrict__ dstat) {
   constexpr int CHEB_SUB = SUB, CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
   constexpr int CHEB_NINT = Cheb<SUB>::NINT, TABLE_D = Cheb<SUB>::TABLE_D;
   static_assert(CHEB_SUB * CHEB_N <= 32, "one lane per node of an octave");
-  static_assert(CHEB_NINT * CHEB_N >= 8 * 2 * QCAP, "quadrature scratch fits in cheb[]");
+  static_assert(CHEB_NINT * CHEB_N >= (TABLE_NT / 32) * 2 * QCAP, "quadrature scratch fits in cheb[]");
   const int k = k0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const PointConst P = pc[k];
@@ -226,9 +245,9 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   __shared__ double cosm[CHEB_N * CHEB_N];  // cosm[j][i] = cos(π j (i + ½) / N), the DCT-II matrix
   if (tid < 16) etab[tid] = kExp2Tab[tid];
   if (tid == 0) next_oct = 0;
-  for (int e = tid; e < CHEB_N * CHEB_N; e += 256) {
+  for (int e = tid; e < CHEB_N * CHEB_N; e += TABLE_NT) {
     tco[e] = SUB == 1 ? kTco1.v[e] : kTco2.v[e];
-    cosm[e] = cospi((e / CHEB_N) * ((e % CHEB_N) + 0.5) / CHEB_N);
+    cosm[e] = SUB == 1 ? g_cosm1[e] : g_cosm2[e];
   }
   // This point's s = 8κ·|Q h|² lies in [8κ·d²min/φ²max, 8κ·d²max/φ²min] (the singular
   // values of the anisotropy map Q are 1/φX, 1/φY): only those octaves, widened by
@@ -285,7 +304,7 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
         double sn;
         if (is_node) {
           const int part = slot / CHEB_N, i = slot % CHEB_N;
-          sn = ldexp(1.0 + (double)part / CHEB_SUB + (0.5 / CHEB_SUB) * (1.0 + cospi((i + 0.5) / CHEB_N)), e);
+          sn = ldexp(1.0 + (double)part / CHEB_SUB + (0.5 / CHEB_SUB) * (1.0 + cosm[CHEB_N + i]), e);
         } else {
           sn = ldexp(1.0 + (double)min(eix, CHEB_SUB) / CHEB_SUB, e);
         }
@@ -345,15 +364,15 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   }
   __syncthreads();
   // detrend: g = ln ρ − L_iv(x), L_iv the line through the interval's edge values
-  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
+  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += TABLE_NT) {
     const int iv = idx / CHEB_N, i = idx % CHEB_N;
-    const double xc = cospi((i + 0.5) / CHEB_N);
+    const double xc = cosm[CHEB_N + i];  // cos(π (i + ½) / N)
     f[idx] -= 0.5 * (edge[iv] + edge[iv + 1]) + 0.5 * (edge[iv + 1] - edge[iv]) * xc;
   }
   __syncthreads();
   // Chebyshev coefficients of g (DCT-II), then monomial coefficients in t (T_j has
   // integer coefficients, exact in FP64) so the build evaluates a plain Horner scheme.
-  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += 256) {
+  for (int idx = olo * CHEB_SUB * CHEB_N + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_N; idx += TABLE_NT) {
     const int iv = idx / CHEB_N, jj = idx % CHEB_N;
     double cc = 0.0;
     if (CHEB_ELO + iv / CHEB_SUB < ez) {
@@ -366,7 +385,7 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
   // monomial coefficients of log2 ρ = log2(e)·(line + Σ c_j T_j(t)); the octave e_zero
   // (if built) holds the constant −2000, which the build's 2^y flushes to 0
   double* T = table + (size_t)blockIdx.x * TABLE_D;
-  for (int idx = olo * CHEB_SUB * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_STRIDE; idx += 256) {
+  for (int idx = olo * CHEB_SUB * CHEB_STRIDE + tid; idx < (ohi + 1) * CHEB_SUB * CHEB_STRIDE; idx += TABLE_NT) {
     const int iv = idx / CHEB_STRIDE, kk = idx % CHEB_STRIDE;
     double a = 0.0;
     if (CHEB_ELO + iv / CHEB_SUB < ez) {
@@ -384,9 +403,9 @@ __global__ void __launch_bounds__(256) table_kernel(PointConst* __restrict__ pc,
 cudaError_t launch_table(int sub, PointConst* pc, int k0, int kw, double* table, const double* dstat,
                          cudaStream_t st) {
   if (sub == 2)
-    table_kernel<2><<<kw, 256, 0, st>>>(pc, k0, table, dstat);
+    table_kernel<2><<<kw, TABLE_NT, 0, st>>>(pc, k0, table, dstat);
   else
-    table_kernel<1><<<kw, 256, 0, st>>>(pc, k0, table, dstat);
+    table_kernel<1><<<kw, TABLE_NT, 0, st>>>(pc, k0, table, dstat);
   return cudaGetLastError();
 }
 

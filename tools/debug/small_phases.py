@@ -1,5 +1,5 @@
 """Per-phase cycle breakdown of chol_small (debug build with LIK_PHASE_TIMERS), for the
-lead warp and warp 0.  usage: python tools/debug/small_phases.py [C2|swiss] [K]"""
+lead warp, warp 0 (update group U) and warp NW-4 (a panel helper).  usage: python tools/debug/small_phases.py [C2|swiss] [K]"""
 import ctypes, os, sys
 sys.path.insert(0, '.')
 os.environ["LIK_LIBRARY"] = os.path.abspath(os.environ.get("PHASE_LIB", "paper_2305_04318_b200/liblik_phase.so"))
@@ -15,15 +15,19 @@ else:
     coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
 ctx = lik.create(0)
 L = lik.lib()
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 36)()
 args = [torch.tensor(a, device="cuda") for a in (coords, y, X, P, lam)]
 ctx.eval_batch_device(*args); torch.cuda.synchronize()
 L.lik_debug_small_phase_cycles(buf, 1)
 ctx.eval_batch_device(*args); torch.cuda.synchronize()
 L.lik_debug_small_phase_cycles(buf, 1)
-v = np.array(list(buf[:16]), dtype=float).reshape(2, 8)
-names = ["load", "build", "factor0+bar", "(lead: G work before factor8)", "(lead: factor8)", "step work", "step barrier", "epilogue"]
-for w, lab in ((0, "lead warp"), (1, "warp 0")):
+v = np.array(list(buf[:36]), dtype=float).reshape(3, 12)
+names = ["load", "build", "panel 0", "G: next-panel update", "G: after the named barrier (helpers: row solves)",
+         "U: trailing update", "step barrier", "epilogue", "G: before the named barrier (lead: factor8s)",
+         "G: named-barrier wait", "-", "-"]
+# (a BAR.SYNC blocks the warp at a later instruction than the clock read after it, so a
+# barrier's wait can show up in the phase after it)
+for w, lab in ((0, "lead warp"), (1, "warp 0 (U)"), (2, "warp NW-4 (a panel helper)")):
     tot = v[w].sum()
     print(f"--- {lab}: total {tot / K / 1e3:.2f} kcyc/point")
     for i, nm in enumerate(names):
