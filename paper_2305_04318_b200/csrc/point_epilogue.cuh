@@ -32,7 +32,8 @@ __device__ inline void point_failure(const CholArgs& A, int k, int code, int tid
 }
 
 // Steps 5-8 from the cross products ssqYX = BᵀV⁻¹B (Cm: r×r, row-major, stride ldc,
-// full), log|V| = logdet (valid in thread lead_tid): XᵀV⁻¹X = QQᵀ (Step 5, pivot ≤
+// full), log|V| = logdet (valid in thread lead_tid): XᵀV⁻¹X = QQᵀ (Step 5; Q's
+// diagonal is stored as 1/Q_cc; pivot ≤
 // p·ε·max diag ⇒ XVX_NOT_PD), c = Q⁻¹XᵀV⁻¹y' (Step 6), ssqBetahat = cᵀc (Step 7),
 // q = y'ᵀV⁻¹y' − ssqBetahat (Step 8; R12), β̂ = Q⁻ᵀc, σ̂² = q/n, ℓ_p, and the optional
 // Table-1 / REML outputs.  Q: p×p scratch (stride ldq); scratch: NULL or 2·p·min(M, nthr)
@@ -57,19 +58,21 @@ __device__ inline void point_epilogue(const CholArgs& A, int k, const double* Cm
         bad = 1;
         break;
       }
-      const double l = sqrt(d);
-      Q[c * ldq + c] = l;
+      // the diagonal holds 1/Q_cc (every later use multiplies by it: no division on the
+      // per-λ chains)
+      const double rl = rsqrt(d);
+      Q[c * ldq + c] = rl;
       for (int i = c + 1; i < p; ++i) {
         double s = Cm[(M + i) * ldc + (M + c)];
         for (int kk = 0; kk < c; ++kk) s -= Q[i * ldq + kk] * Q[c * ldq + kk];
-        Q[i * ldq + c] = s / l;
+        Q[i * ldq + c] = s * rl;
       }
     }
     flag[1] = bad;
     scal[1] = logdet;  // log|V| = Σ log pivots (Step 2)
     double ldx = 0.0;  // log|XᵀV⁻¹X| = 2 Σ log Q_cc (Step 5, Table 1 detReml)
     if (!bad)
-      for (int c = 0; c < p; ++c) ldx += 2.0 * log(Q[c * ldq + c]);
+      for (int c = 0; c < p; ++c) ldx -= 2.0 * log(Q[c * ldq + c]);
     scal[2] = ldx;
   }
   __syncthreads();
@@ -92,7 +95,7 @@ __device__ inline void point_epilogue(const CholArgs& A, int k, const double* Cm
     for (int a = 0; a < p; ++a) {  // Step 6: c = Q⁻¹ XᵀV⁻¹y'
       double s = Cm[(M + a) * ldc + m];
       for (int b = 0; b < a; ++b) s -= Q[a * ldq + b] * cv[b];
-      cv[a] = s / Q[a * ldq + a];
+      cv[a] = s * Q[a * ldq + a];
       sb += cv[a] * cv[a];  // Step 7: ssqBetahat = cᵀc
     }
     const double yy = Cm[m * ldc + m];
@@ -104,7 +107,7 @@ __device__ inline void point_epilogue(const CholArgs& A, int k, const double* Cm
     for (int a = p - 1; a >= 0; --a) {  // β̂ = Q⁻ᵀ c (Eq. betahat)
       double s = cv[a];
       for (int b = a + 1; b < p; ++b) s -= Q[b * ldq + a] * bt[b];
-      bt[a] = s / Q[a * ldq + a];
+      bt[a] = s * Q[a * ldq + a];
     }
     const size_t km = (size_t)k * M + m;
     if (A.ssqBetahat) A.ssqBetahat[km] = sb;
