@@ -217,11 +217,13 @@ __device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
 // A = κ(x − (e^x − 1)) and B = e^{−x}/(4κ) once (into shared memory), so each lane's
 // G(x; s) = A − s·B costs one FMA and its term one exp.
 // ---------------------------------------------------------------------------
-constexpr int QCAP = 64;  // grid nodes per warp chunk
 #ifndef LIK_TABLE_NT
 #define LIK_TABLE_NT 256  // threads per point (the octaves are spread over its warps)
 #endif
 constexpr int TABLE_NT = LIK_TABLE_NT;
+#ifndef LIK_TABLE_UOCT
+#define LIK_TABLE_UOCT 3  // octaves per shared quadrature grid in the whole-octave layout
+#endif
 
 template <int SUB>
 __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict__ pc, int k0,
@@ -229,8 +231,6 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
                                                     const double* __restrict__ dstat) {
   constexpr int CHEB_SUB = SUB, CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
   constexpr int CHEB_NINT = Cheb<SUB>::NINT, TABLE_D = Cheb<SUB>::TABLE_D;
-  static_assert(CHEB_SUB * CHEB_N <= 32, "one lane per node of an octave");
-  static_assert(CHEB_NINT * CHEB_N >= (TABLE_NT / 32) * 2 * QCAP, "quadrature scratch fits in cheb[]");
   const int k = k0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const PointConst P = pc[k];
@@ -263,22 +263,34 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
   // · (1 + (iv mod SUB)/SUB) (edge), all from the octave's shared quadrature grid
   {
     const double kap = P.kappa, i4k = P.inv4k;
+    constexpr int QCAP = (CHEB_NINT * CHEB_N / (TABLE_NT / 32) / 2) / 32 * 32;  // grid chunk (scratch in cheb[])
+    static_assert(QCAP >= 64, "grid scratch");
     double* qa = cheb + warp * 2 * QCAP;
     double* qb = qa + QCAP;
     constexpr int NODES = CHEB_SUB * CHEB_N;
-    constexpr int NPASS = NODES + CHEB_SUB + 1 <= 32 ? 1 : 2;  // node lanes, then the edge lanes
-    // octaves handed out dynamically (their grids differ a lot in length); each octave's
-    // values do not depend on which warp computes them
+    // a unit of UOCT consecutive octaves shares one quadrature grid: its slots are, per
+    // octave, the NODES Chebyshev nodes and the SUB lower interval edges, then the top
+    // edge of the unit's last octave (kept only at ohi, else it is the next unit's first
+    // edge).  SUB = 1: 3 × 21 + 1 = 64 slots = two passes with every lane busy (one octave
+    // per warp left 10 of 32 lanes idle), and the window search, the grid and the per-octave
+    // setup once per three octaves; the grid of a unit is ~10 % longer than an octave's.
+    constexpr int UOCT = CHEB_SUB == 1 ? LIK_TABLE_UOCT : 1;
+    constexpr int PER = NODES + CHEB_SUB;
+    constexpr int NSLOT = UOCT * PER + 1;
+    constexpr int NPASS = (NSLOT + 31) / 32;
+    // units handed out dynamically (their grids differ a lot in length); each unit's values
+    // do not depend on which warp computes them (units start at olo + UOCT·u)
     for (;;) {
-      int o = 0;
-      if (lane == 0) o = olo + atomicAdd(&next_oct, 1);
-      o = __shfl_sync(0xffffffffu, o, 0);
-      if (o > ohi) break;
-      const int e = CHEB_ELO + o;
-      const double s0 = ldexp(1.0, e), s1 = 2.0 * s0;
+      int o0 = 0;
+      if (lane == 0) o0 = olo + atomicAdd(&next_oct, UOCT);
+      o0 = __shfl_sync(0xffffffffu, o0, 0);
+      if (o0 > ohi) break;
+      const int nu = min(UOCT, ohi - o0 + 1);  // octaves in this unit
+      const int e = CHEB_ELO + o0;
+      const double s0 = ldexp(1.0, e), s1 = ldexp(1.0, e + nu);
       double x0, x1, h0, h;
       quad_peak_step(kap, s0, x0, h0);
-      quad_peak_step(kap, s1, x1, h);
+      quad_peak_step(kap, s1, x1, h);  // the finest step of the unit
       const double a0 = s0 * i4k, a1 = s1 * i4k;
       const double g0 = quad_G(kap, a0, x0), g1 = quad_G(kap, a1, x1);
       // left extent from the peak of s0, right extent from the peak of s1
@@ -296,17 +308,22 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
       const double xl = x0 - L * h;
       const int nq = L + (int)ceil((x1 - x0) / h) + R + 1;
       for (int pass = 0; pass < NPASS; ++pass) {
-        // this lane's s: a Chebyshev node (slot < NODES) or an interval edge
-        const int slot = NPASS == 1 ? lane : (pass == 0 ? lane : NODES + lane);
-        const bool is_node = slot < NODES;
-        const int eix = slot - NODES;  // edge index within the octave: 0..SUB (SUB = the top edge)
-        const bool active = is_node || (eix <= CHEB_SUB && (eix < CHEB_SUB || o == ohi));
+        // this lane's s: a Chebyshev node or a lower interval edge of octave o = o0 + oo
+        // (oo < nu), or the unit's top edge (slot nu·PER: the lower edge of octave o0 + nu,
+        // kept only when the unit ends at ohi)
+        const int slot = pass * 32 + lane;
+        const int oo = slot / PER, w = slot % PER;
+        const int o = o0 + oo;
+        const bool in_oct = oo < nu;
+        const bool is_node = in_oct && w < NODES;
+        const int eix = in_oct ? w - NODES : 0;
+        const bool active = in_oct || (slot == nu * PER && o0 + nu - 1 == ohi);
         double sn;
         if (is_node) {
-          const int part = slot / CHEB_N, i = slot % CHEB_N;
-          sn = ldexp(1.0 + (double)part / CHEB_SUB + (0.5 / CHEB_SUB) * (1.0 + cosm[CHEB_N + i]), e);
+          const int part = w / CHEB_N, i = w % CHEB_N;
+          sn = ldexp(1.0 + (double)part / CHEB_SUB + (0.5 / CHEB_SUB) * (1.0 + cosm[CHEB_N + i]), CHEB_ELO + o);
         } else {
-          sn = ldexp(1.0 + (double)min(eix, CHEB_SUB) / CHEB_SUB, e);
+          sn = ldexp(1.0 + (double)max(eix, 0) / CHEB_SUB, CHEB_ELO + o);
         }
         double xs, hs;
         quad_peak_step(kap, sn, xs, hs);
@@ -338,11 +355,13 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
         }
         __syncwarp();
         const double lr = P.lnC + gs + log(h * sum);
-        if (is_node) {
-          const int part = slot / CHEB_N, i = slot % CHEB_N;
-          f[(o * CHEB_SUB + part) * CHEB_N + i] = lr;
-        } else if (active) {
-          edge[o * CHEB_SUB + eix] = lr;
+        if (active) {
+          if (is_node) {
+            const int part = w / CHEB_N, i = w % CHEB_N;
+            f[(o * CHEB_SUB + part) * CHEB_N + i] = lr;
+          } else {
+            edge[o * CHEB_SUB + eix] = lr;  // (the top edge: octave o0 + nu, eix 0)
+          }
         }
       }
     }
