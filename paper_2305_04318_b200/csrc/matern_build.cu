@@ -208,12 +208,12 @@ __device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
 // degree 19 resp. 15 reaches the FP64 rounding floor (~1e-16·max(1, |ln ρ|)),
 // DESIGN.md §5.
 //
-// The nodes of one octave share a quadrature grid: one warp per octave, one lane
-// per Chebyshev node (SUB = 2: 2 × 16 = 32 lanes; SUB = 1: 20).  The grid step is
-// the one of the octave's largest s (the finest: the peak's curvature κr grows with
-// s), and the grid spans the union of the nodes' windows — from where G(·; 2^e)
-// falls 40 below its peak on the left (the smallest s has the longest left tail) to
-// where G(·; 2^{e+1}) does on the right.  Per grid node the warp computes
+// The nodes of a unit of octaves (three for SUB = 1, one for SUB = 2) share a quadrature
+// grid: one warp per unit, one lane per node or interval edge (SUB = 1: 3 × (20 + 1) + 1
+// = 64 = two passes of 32 lanes).  The grid step is the one of the unit's largest s (the
+// finest: the peak's curvature κr grows with s), and the grid spans the union of the
+// nodes' windows — from where G(·; s_min) falls 40 below its peak on the left (the
+// smallest s has the longest left tail) to where G(·; s_max) does on the right.  Per grid node the warp computes
 // A = κ(x − (e^x − 1)) and B = e^{−x}/(4κ) once (into shared memory), so each lane's
 // G(x; s) = A − s·B costs one FMA and its term one exp.
 // ---------------------------------------------------------------------------
