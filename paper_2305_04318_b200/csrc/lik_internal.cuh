@@ -104,18 +104,22 @@ struct PointConst {
 // 2^e_zero ρ = 0: the interval of the octave e_zero holds the constant −2000 (2^−2000
 // flushes to 0), and the build clamps every larger s to it.
 // Two table layouts, chosen per call from n (cheb_sub_for): SUB = 1 whole octaves
-// with degree 19; SUB = 2 splits every octave at its linear midpoint ([1, 1.5) and
-// [1.5, 2) × 2^e; interval = SUB·octave + the top mantissa bit of s) with degree
-// 15 — the worse half sees the branch point at s = 0 from 5 half-widths (Bernstein
-// ρ = 9.9 vs 5.8), so the truncation stays at the same ~1e-16 level.  Halves cost
-// the table kernel 1.6× the exact evaluations per point and save the build 4 DFMA
-// and 2 LDS.128 per element, so they pay from a few hundred sites on.
+// with degree 19; SUB = CHEB_SUB_LARGE = 4 splits every octave into quarters
+// ([1, 1.25), …, [1.75, 2) × 2^e; interval = SUB·octave + the top two mantissa bits of
+// s) with degree 11 — the worst quarter sees the branch point at s = 0 from 9
+// half-widths (Bernstein ρ = 17.9 vs 5.8), so the truncation stays ≤ 2e-17·max(1,
+// |ln ρ|).  Quarters cost the table kernel 2.4× the exact evaluations per point and save
+// the build 8 DFMA and 4 LDS.128 per element against whole octaves (C4 build −9 %
+// against halves with degree 15), so they pay from a few hundred sites on.
 constexpr int CHEB_ELO = -52;
 constexpr int CHEB_NOCT = 80;
 template <int SUB>
 struct Cheb {
-  static_assert(SUB == 1 || SUB == 2, "intervals per octave");
-  static constexpr int N = SUB == 1 ? 20 : 16;  // coefficients per interval
+  static_assert(SUB == 1 || SUB == 2 || SUB == 4 || SUB == 8, "intervals per octave");
+  static constexpr int LOG2SUB = SUB == 1 ? 0 : SUB == 2 ? 1 : SUB == 4 ? 2 : 3;
+  // coefficients per interval: the truncation of the worst interval [1, 1 + 1/SUB)·2^e
+  // stays ≤ 2e-17·max(1, |ln ρ|) (mpmath, κ ∈ [0.2, 200]), far below the rounding floor
+  static constexpr int N = SUB == 1 ? 20 : SUB == 2 ? 16 : SUB == 4 ? 12 : 10;
   // + 2 pad doubles: consecutive intervals start 16 bytes (4 banks) apart, so lanes of a
   // warp reading the same pair of different intervals hit different banks (a stride of
   // a multiple of 128 bytes serialises them: build 1.6× slower, measured)
@@ -123,11 +127,17 @@ struct Cheb {
   static constexpr int NINT = CHEB_NOCT * SUB;  // intervals
   static constexpr int TABLE_D = STRIDE * NINT;
 };
-constexpr int TABLE_D = Cheb<1>::TABLE_D > Cheb<2>::TABLE_D ? Cheb<1>::TABLE_D : Cheb<2>::TABLE_D;
+// the layout for n ≥ LIK_CHEB_SUB_MIN_N (the whole-octave layout below)
+#ifndef LIK_CHEB_SUB_LARGE
+#define LIK_CHEB_SUB_LARGE 4
+#endif
+constexpr int CHEB_SUB_LARGE = LIK_CHEB_SUB_LARGE;
+constexpr int TABLE_D = Cheb<1>::TABLE_D > Cheb<CHEB_SUB_LARGE>::TABLE_D ? Cheb<1>::TABLE_D
+                                                                         : Cheb<CHEB_SUB_LARGE>::TABLE_D;
 #ifndef LIK_CHEB_SUB_MIN_N
 #define LIK_CHEB_SUB_MIN_N 256
 #endif
-inline int cheb_sub_for(int n) { return n >= LIK_CHEB_SUB_MIN_N ? 2 : 1; }
+inline int cheb_sub_for(int n) { return n >= LIK_CHEB_SUB_MIN_N ? CHEB_SUB_LARGE : 1; }
 
 // Launch wrappers (defined in the .cu files).  All enqueue on `st`.
 // prep: Box-Cox rows of Bᵀ, S = Σ log y, and the site gather coords_p[i] = coords[perm[i]]

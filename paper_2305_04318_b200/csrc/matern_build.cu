@@ -179,22 +179,28 @@ constexpr TcoTable<N> make_tco() {
       t.v[jj * N + kk] = (kk > 0 ? 2.0 * t.v[(jj - 1) * N + kk - 1] : 0.0) - t.v[(jj - 2) * N + kk];
   return t;
 }
-// The DCT-II matrices cos(π j (i + ½) / N) of both layouts, written once per process by
-// cheb_init_kernel (lik_create) instead of 400 cospi per point in every table block.
-__device__ double g_cosm1[Cheb<1>::N * Cheb<1>::N];
-__device__ double g_cosm2[Cheb<2>::N * Cheb<2>::N];
+// The DCT-II matrices cos(π j (i + ½) / N) of the table layouts, written once per process
+// by cheb_init_kernel (lik_create) instead of N² cospi per point in every table block.
+template <int N>
+struct CosTable {
+  double v[N * N];
+};
+__device__ CosTable<Cheb<1>::N> g_cosm1;
+__device__ CosTable<Cheb<CHEB_SUB_LARGE>::N> g_cosmL;
+template <int N>
+__device__ void fill_cos(CosTable<N>& t) {
+  for (int e = threadIdx.x; e < N * N; e += blockDim.x) t.v[e] = cospi((e / N) * ((e % N) + 0.5) / N);
+}
 __global__ void cheb_init_kernel() {
-  for (int e = threadIdx.x; e < Cheb<1>::N * Cheb<1>::N; e += blockDim.x)
-    g_cosm1[e] = cospi((e / Cheb<1>::N) * ((e % Cheb<1>::N) + 0.5) / Cheb<1>::N);
-  for (int e = threadIdx.x; e < Cheb<2>::N * Cheb<2>::N; e += blockDim.x)
-    g_cosm2[e] = cospi((e / Cheb<2>::N) * ((e % Cheb<2>::N) + 0.5) / Cheb<2>::N);
+  fill_cos(g_cosm1);
+  fill_cos(g_cosmL);
 }
 cudaError_t launch_cheb_init(cudaStream_t st) {
   cheb_init_kernel<<<1, 256, 0, st>>>();
   return cudaGetLastError();
 }
 __device__ const TcoTable<Cheb<1>::N> kTco1 = make_tco<Cheb<1>::N>();
-__device__ const TcoTable<Cheb<2>::N> kTco2 = make_tco<Cheb<2>::N>();
+__device__ const TcoTable<Cheb<CHEB_SUB_LARGE>::N> kTcoL = make_tco<Cheb<CHEB_SUB_LARGE>::N>();
 
 // ---------------------------------------------------------------------------
 // table: one block per point of the wave.  ln ρ is evaluated exactly (the
@@ -235,8 +241,9 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const PointConst P = pc[k];
   if (P.mode != MODE_BESSEL) return;
-  __shared__ double f[CHEB_NINT * CHEB_N];
-  __shared__ double cheb[CHEB_NINT * CHEB_N];  // also the warps' quadrature scratch
+  extern __shared__ double tsm[];  // dynamic: f and cheb (CHEB_NINT·CHEB_N doubles each)
+  double* f = tsm;
+  double* cheb = tsm + CHEB_NINT * CHEB_N;  // also the warps' quadrature scratch
   __shared__ double edge[CHEB_NINT + 1];
   __shared__ int ez, next_oct;
   __shared__ double etab[16];
@@ -246,8 +253,13 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
   if (tid < 16) etab[tid] = kExp2Tab[tid];
   if (tid == 0) next_oct = 0;
   for (int e = tid; e < CHEB_N * CHEB_N; e += TABLE_NT) {
-    tco[e] = SUB == 1 ? kTco1.v[e] : kTco2.v[e];
-    cosm[e] = SUB == 1 ? g_cosm1[e] : g_cosm2[e];
+    if constexpr (SUB == 1) {
+      tco[e] = kTco1.v[e];
+      cosm[e] = g_cosm1.v[e];
+    } else {
+      tco[e] = kTcoL.v[e];
+      cosm[e] = g_cosmL.v[e];
+    }
   }
   // This point's s = 8κ·|Q h|² lies in [8κ·d²min/φ²max, 8κ·d²max/φ²min] (the singular
   // values of the anisotropy map Q are 1/φX, 1/φY): only those octaves, widened by
@@ -421,11 +433,15 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
 
 cudaError_t launch_table(int sub, PointConst* pc, int k0, int kw, double* table, const double* dstat,
                          cudaStream_t st) {
-  if (sub == 2)
-    table_kernel<2><<<kw, TABLE_NT, 0, st>>>(pc, k0, table, dstat);
-  else
-    table_kernel<1><<<kw, TABLE_NT, 0, st>>>(pc, k0, table, dstat);
-  return cudaGetLastError();
+  auto go = [&](auto kern, int nint_n) -> cudaError_t {
+    const int smem = 2 * nint_n * (int)sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<kw, TABLE_NT, smem, st>>>(pc, k0, table, dstat);
+    return cudaGetLastError();
+  };
+  if (sub == CHEB_SUB_LARGE) return go(table_kernel<CHEB_SUB_LARGE>, Cheb<CHEB_SUB_LARGE>::NINT * Cheb<CHEB_SUB_LARGE>::N);
+  return go(table_kernel<1>, Cheb<1>::NINT * Cheb<1>::N);
 }
 
 // ---------------------------------------------------------------------------
@@ -567,8 +583,8 @@ cudaError_t launch_build(int sub, const double* coords, const SlotGeom& g, const
                          double* ws, cudaStream_t st) {
   const cudaTextureObject_t tex = table_tex;
   dim3 grid((g.ntri + g.nt + BUILD_TILES - 1) / BUILD_TILES, kw);
-  if (sub == 2)
-    build_kernel<2><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
+  if (sub == CHEB_SUB_LARGE)
+    build_kernel<CHEB_SUB_LARGE><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
   else
     build_kernel<1><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
   return cudaGetLastError();

@@ -149,6 +149,10 @@ __device__ __forceinline__ double exp2_neg(double y, const double* etab) {
   return m >= -1021 ? out : 0.0;
 }
 
+// High word of the first interval's centre 2^{LG+1} + 1 (3, 5, 9, 17 for SUB = 1, 2, 4, 8);
+// interval `part` adds 2·part, i.e. part << (20 − LG) in the high word.
+constexpr int centre_hi(int lg) { return ((1023 + lg + 1) << 20) | (1 << (20 - lg - 1)); }
+
 // Table evaluation of NE elements, interleaved (independent Horner chains for ILP).
 // s = z² from the point's scaled rotation (no square root); the octave o of s is
 // clamped to [olo, oz] (oz: the underflow octave, or ohi); elements whose octave lies
@@ -162,7 +166,8 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
                                                   const double* etab, int olo, int oz, unsigned span,
                                                   const double (&hx)[NE], const double (&hy)[NE],
                                                   double (&v)[NE], unsigned& slow, int bit) {
-  constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
+  constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE, LG = Cheb<SUB>::LOG2SUB;
+  constexpr int kCentreHi = centre_hi(LG);
   double t[NE], h[NE];
   const double2* cp[NE];
 #pragma unroll
@@ -175,14 +180,14 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
       const int o = (hi >> 20) - (1023 + CHEB_ELO);
       slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
     }
-    // interval = SUB·octave + the top mantissa bit (SUB = 2): one shift of the high word;
+    // interval = SUB·octave + the top log2(SUB) mantissa bits: one shift of the high word;
     // clamped to [SUB·olo, SUB·oz + SUB − 1] (above: the underflow octave's constant)
-    const int iv = min(max((hi >> (21 - SUB)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
-    // t ∈ [−1, 1) from the mantissa alone: 2^{SUB}·(1.mantissa) (exponent field set to
-    // 1023 + SUB) minus the interval's centre 2·SUB + 1 + 2·part — exact
-    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + SUB) << 20), __double2loint(sv));
-    const int part = SUB == 1 ? 0 : (hi >> 19) & 1;
-    const double centre = __hiloint2double((SUB == 1 ? 0x40080000 : 0x40140000) + (part << 19), 0);  // 3 | 5 or 7
+    const int iv = min(max((hi >> (20 - LG)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
+    // t ∈ [−1, 1) from the mantissa alone: 2^{LG+1}·(1.mantissa) (exponent field set to
+    // 1023 + LG + 1) minus the interval's centre 2^{LG+1} + 1 + 2·part — exact
+    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + LG + 1) << 20), __double2loint(sv));
+    const int part = (hi >> (20 - LG)) & (SUB - 1);
+    const double centre = __hiloint2double(kCentreHi + (part << (20 - LG)), 0);
     t[e] = m4 - centre;
     cp[e] = reinterpret_cast<const double2*>(coef + iv * CHEB_STRIDE);
   }
@@ -240,7 +245,8 @@ __device__ __forceinline__ void matern_rho_tableN_tex(const PointConst& P, cudaT
                                                       int oz, unsigned span, const double (&hx)[NE],
                                                       const double (&hy)[NE], double (&v)[NE],
                                                       unsigned& slow, int bit) {
-  constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE;
+  constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE, LG = Cheb<SUB>::LOG2SUB;
+  constexpr int kCentreHi = centre_hi(LG);
   double t[NE], h[NE];
   long long cp[NE];
   int ci[NE];
@@ -254,10 +260,10 @@ __device__ __forceinline__ void matern_rho_tableN_tex(const PointConst& P, cudaT
       const int o = (hi >> 20) - (1023 + CHEB_ELO);
       slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
     }
-    const int iv = min(max((hi >> (21 - SUB)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
-    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + SUB) << 20), __double2loint(sv));
-    const int part = SUB == 1 ? 0 : (hi >> 19) & 1;
-    const double centre = __hiloint2double((SUB == 1 ? 0x40080000 : 0x40140000) + (part << 19), 0);
+    const int iv = min(max((hi >> (20 - LG)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
+    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + LG + 1) << 20), __double2loint(sv));
+    const int part = (hi >> (20 - LG)) & (SUB - 1);
+    const double centre = __hiloint2double(kCentreHi + (part << (20 - LG)), 0);
     t[e] = m4 - centre;
     cp[e] = tbase + (long long)iv * (CHEB_STRIDE / 2);
     ci[e] = iv * CHEB_STRIDE;
