@@ -1,6 +1,6 @@
 """A/B timing of the small-matrix path: ms per lik_eval_batch_device call on C2 (n = 200,
 1,000 points × 5 λ) and the paper's Swiss shape (n = 100, p = 2, 15,318 points × 34 λ),
-CUDA events around 20 calls after 5 warm-up calls, for each library given (LIK_LIBRARY
+CUDA events around 20 calls after 5 warm-up calls (and through a prepared lik_dataset), for each library given (LIK_LIBRARY
 per process: run one process per library).  usage: python tools/small_ab.py [C2|swiss ...]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -27,4 +27,17 @@ for name in sys.argv[1:] or ["C2", "swiss"]:
     e1.record()
     torch.cuda.synchronize()
     res.append(f"{name} {e0.elapsed_time(e1) / 20:.3f} ms")
+    # the prepare-once dataset path (validation and site ordering done once)
+    ds = ctx.dataset(*arrs[:3], arrs[4])
+    out = None
+    for _ in range(5):
+        out = ds.eval_device(t[3], out=out)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        ds.eval_device(t[3], out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ds.close()
+    res[-1] += f" (dataset {e0.elapsed_time(e1) / 20:.3f} ms)"
 print(os.path.basename(os.environ.get("LIK_LIBRARY", "liblik.so")), " | ".join(res))
