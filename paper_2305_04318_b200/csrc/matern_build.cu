@@ -460,6 +460,9 @@ constexpr int BUILD_TILES = LIK_BUILD_TILES;  // tiles of one point per block (a
 #endif
 constexpr int BUILD_NE = LIK_BUILD_NE;  // elements per thread evaluated interleaved (2 or 4)
 
+#ifndef LIK_BUILD_VEC
+#define LIK_BUILD_VEC 0  // 1: two columns per thread, 16-byte stores
+#endif
 #ifndef LIK_BUILD_MINB
 #define LIK_BUILD_MINB 4  // 64 registers, 4 blocks (32 warps) per SM: 36.8 vs 40.6 ms per 2,960 C4 points
 #endif
@@ -488,10 +491,19 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
     for (int e = olo * SUB * CHEB_STRIDE / 2 + threadIdx.x; e < (oz + 1) * SUB * CHEB_STRIDE / 2; e += 256)
       dst[e] = src[e];
   }
+#if LIK_BUILD_VEC
+  // thread -> columns c, c + 1 (c even), rows r0 + 8q (q < 8): a warp covers the 64
+  // columns of one row, and each element pair (c, c + 1) of a row leaves as one 16-byte
+  // store (the swizzle XORs multiples of 4 into the column: pairs stay adjacent)
+  const int c = 2 * (threadIdx.x & 31), r0 = threadIdx.x >> 5;
+  constexpr int RSTEP = 8, NQ = 8;
+#else
   // thread -> column c, rows r0 + 4q (q < 16): a warp covers 32 consecutive
   // columns of one row; with Morton-ordered sites their s values mostly share an
   // interval, so the coefficient loads are shared-memory broadcasts.
   const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
+  constexpr int RSTEP = 4, NQ = 16;
+#endif
   for (int tt = 0; tt < BUILD_TILES; ++tt) {
     const int tile = blockIdx.x * BUILD_TILES + tt;
     if (tile >= g.ntri + g.nt) break;
@@ -516,63 +528,87 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
       sxy[side][l] = gi < g.n ? reinterpret_cast<const double2*>(coords)[gi] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const double2 cj = sxy[1][c];
     const bool regular = (i > j) && ((i + 1) * TB <= g.n);
-    // the thread's 16 rows r0 + 4q share the swizzle of r0 (rows differ by multiples of 4)
+    // the thread's rows r0 + RSTEP·q share the swizzle of r0 (rows differ by multiples of 4)
     double* Tc = T + sw_off(r0, c);
-    unsigned slow = 0u;
+    unsigned slow = 0u;  // bit = element index of the thread (row-major over its rows × columns)
+#if LIK_BUILD_VEC
+    const double2 cj0 = sxy[1][c], cj1 = sxy[1][c + 1];
+#else
+    const double2 cj = sxy[1][c];
+#endif
     if (P.mode == MODE_BESSEL) {
 #pragma unroll 2
-      for (int q = 0; q < 16; q += BUILD_NE) {
+      for (int q = 0; q < NQ; q += BUILD_NE / (LIK_BUILD_VEC ? 2 : 1)) {
         double hx[BUILD_NE], hy[BUILD_NE], v[BUILD_NE];
 #pragma unroll
         for (int e = 0; e < BUILD_NE; ++e) {
-          const double2 ri = sxy[0][r0 + 4 * (q + e)];
+#if LIK_BUILD_VEC
+          const double2 ri = sxy[0][r0 + RSTEP * (q + (e >> 1))];
+          const double2 cj = (e & 1) ? cj1 : cj0;
+#else
+          const double2 ri = sxy[0][r0 + RSTEP * (q + e)];
+#endif
           hx[e] = ri.x - cj.x;
           hy[e] = ri.y - cj.y;
         }
+        const int bit = LIK_BUILD_VEC ? 2 * q : q;
 #if LIK_BUILD_TEXMASK
         const long long tb = (long long)slot * (TABLE_D / 2);
         if (regular && P.range_ok)
-          matern_rho_tableN_tex<BUILD_NE, SUB, false>(P, tex, tb, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+          matern_rho_tableN_tex<BUILD_NE, SUB, false>(P, tex, tb, coef, etab, olo, oz, span, hx, hy, v, slow, bit);
         else
-          matern_rho_tableN_tex<BUILD_NE, SUB, true>(P, tex, tb, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+          matern_rho_tableN_tex<BUILD_NE, SUB, true>(P, tex, tb, coef, etab, olo, oz, span, hx, hy, v, slow, bit);
 #else
         if (regular && P.range_ok)
-          matern_rho_tableN<BUILD_NE, SUB, false>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+          matern_rho_tableN<BUILD_NE, SUB, false>(P, coef, etab, olo, oz, span, hx, hy, v, slow, bit);
         else
-          matern_rho_tableN<BUILD_NE, SUB, true>(P, coef, etab, olo, oz, span, hx, hy, v, slow, q);
+          matern_rho_tableN<BUILD_NE, SUB, true>(P, coef, etab, olo, oz, span, hx, hy, v, slow, bit);
 #endif
+#if LIK_BUILD_VEC
 #pragma unroll
-        for (int e = 0; e < BUILD_NE; ++e) Tc[(q + e) * 4 * KC] = v[e];
+        for (int e = 0; e < BUILD_NE; e += 2)
+          *reinterpret_cast<double2*>(Tc + (q + e / 2) * RSTEP * KC) = make_double2(v[e], v[e + 1]);
+#else
+#pragma unroll
+        for (int e = 0; e < BUILD_NE; ++e) Tc[(q + e) * RSTEP * KC] = v[e];
+#endif
       }
     } else {
 #pragma unroll 4
-      for (int q = 0; q < 16; ++q) {
-        const double2 ri = sxy[0][r0 + 4 * q];
-        Tc[q * 4 * KC] = exp(-2.0 * aniso_d2(P, ri.x - cj.x, ri.y - cj.y));
+      for (int q = 0; q < NQ; ++q) {
+        const double2 ri = sxy[0][r0 + RSTEP * q];
+#if LIK_BUILD_VEC
+        *reinterpret_cast<double2*>(Tc + q * RSTEP * KC) =
+            make_double2(exp(-2.0 * aniso_d2(P, ri.x - cj0.x, ri.y - cj0.y)),
+                         exp(-2.0 * aniso_d2(P, ri.x - cj1.x, ri.y - cj1.y)));
+#else
+        Tc[q * RSTEP * KC] = exp(-2.0 * aniso_d2(P, ri.x - cj.x, ri.y - cj.y));
+#endif
       }
     }
     if (!regular || slow) {
       // fix-up pass (rewrites): padding, diagonal, unused upper triangle, outside the table
 #pragma unroll 1
-      for (int q = 0; q < 16; ++q) {
-        const int r = r0 + 4 * q;
-        const int gi = i * TB + r, gj = j * TB + c;
+      for (int idx = 0; idx < 16; ++idx) {
+        const int r = r0 + RSTEP * (LIK_BUILD_VEC ? idx >> 1 : idx);
+        const int cc = c + (LIK_BUILD_VEC ? idx & 1 : 0);
+        const int gi = i * TB + r, gj = j * TB + cc;
         double v;
         if (gi >= g.n || gj >= g.n) {
           v = (gi == gj) ? 1.0 : 0.0;
         } else if (gi == gj) {
           v = 1.0 + P.nugget;
-        } else if (i == j && c > r) {
+        } else if (i == j && cc > r) {
           v = 0.0;
-        } else if ((slow >> q) & 1u) {
+        } else if ((slow >> idx) & 1u) {
           const double2 ri = sxy[0][r];
-          v = matern_rho_exact(P, ri.x - cj.x, ri.y - cj.y);
+          const double2 cjj = sxy[1][cc];
+          v = matern_rho_exact(P, ri.x - cjj.x, ri.y - cjj.y);
         } else {
           continue;
         }
-        T[sw_off(r, c)] = v;
+        T[sw_off(r, cc)] = v;
       }
     }
   }
