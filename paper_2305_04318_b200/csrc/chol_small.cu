@@ -48,6 +48,9 @@ __device__ __forceinline__ long long sph_clock() {
 #define SPH_FLUSH(w, slot) do {} while (0)
 #endif
 
+#ifndef LIK_SMALL_PIV2
+#define LIK_SMALL_PIV2 1  // two pivots per step in the 8×8 factorisation (0: one; Swiss −0.7 %, C2 −0.5 %)
+#endif
 #ifndef LIK_SMALL_UCH
 #define LIK_SMALL_UCH 2  // trailing-update tiles per chunk (C2 −6 %, Swiss −4 % against 4: the update competes less with the panel chain)
 #endif
@@ -99,6 +102,40 @@ __device__ __forceinline__ void factor8(const double* Skk, double* Wn, double* p
   double x[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) x[i] = (i == l) ? 1.0 : 0.0;
+#if LIK_SMALL_PIV2
+  // two pivots per step: for the 2×2 block [[d0, e], [e, f]] both reciprocal square roots
+  // (1/L_cc = rsqrt(d0), 1/L_c1c1 = √d0 · rsqrt(d0 f − e²)) issue together, so the
+  // chain carries 4 rsqrt latencies per tile instead of 8
+#define A_(i, j) a[(i) * ((i) + 1) / 2 + (j)]
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) {
+    const int c1 = c + 1;
+    const double d0 = A_(c, c), e = A_(c1, c), f = A_(c1, c1);
+    const double det = fma(d0, f, -e * e);
+    const double r0 = rsqrt(d0), rd = rsqrt(det);
+    const double d1 = det * (r0 * r0);  // the second pivot, det / d0
+    fail |= !(d0 > tol) || !(d1 > tol);
+    if (l == c) mypiv = d0;
+    if (l == c1) mypiv = d1;
+    const double l10 = e * r0;           // L_c1c
+    const double r1 = rd * (d0 * r0);    // 1 / L_c1c1
+#pragma unroll
+    for (int i = c1 + 1; i < 8; ++i) {
+      A_(i, c) *= r0;                                  // L_ic
+      A_(i, c1) = (A_(i, c1) - A_(i, c) * l10) * r1;  // L_ic1
+    }
+#pragma unroll
+    for (int i = c1 + 1; i < 8; ++i)
+#pragma unroll
+      for (int j = c1 + 1; j <= i; ++j) A_(i, j) -= A_(i, c) * A_(j, c) + A_(i, c1) * A_(j, c1);
+    // W column l: forward substitution in axpy form
+    x[c] *= r0;
+    x[c1] = (x[c1] - l10 * x[c]) * r1;
+#pragma unroll
+    for (int i = c1 + 1; i < 8; ++i) x[i] -= A_(i, c) * x[c] + A_(i, c1) * x[c1];
+  }
+#undef A_
+#else
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const double d = a[c * (c + 1) / 2 + c];
@@ -116,6 +153,7 @@ __device__ __forceinline__ void factor8(const double* Skk, double* Wn, double* p
 #pragma unroll
     for (int i = c + 1; i < 8; ++i) x[i] -= a[i * (i + 1) / 2 + c] * x[c];
   }
+#endif
   if (lane < 8) {
 #pragma unroll
     for (int m = 0; m < 8; ++m) Wn[toff(m, l)] = -x[m];
