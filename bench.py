@@ -399,9 +399,10 @@ def main():
         build_ms, build_n = stages["matern_build"]
         peak, peak_src = fp64_peak()
         achieved = (args.steps * K * F) / (chol_ms / 1e3) / 1e12 if chol_ms > 0 else None
-        traffic, traffic_note = None, None
+        traffic, traffic_note, ncu_dmma = None, None, None
         try:
             tj = json.load(open(TRAFFIC))
+            ncu_dmma = tj.get("dmma_pipe_pct")
             if tj.get("n", 2000) == n:
                 pts_per_launch = args.steps * K / chol_n if chol_n else K
                 traffic = tj["dram_bytes_per_point"] * pts_per_launch
@@ -428,6 +429,7 @@ def main():
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "traffic_note": traffic_note,
                          "peak_source": peak_src,
+                         "ncu_dmma_pipe_pct": ncu_dmma,  # the DMMA pipe's busy share in the committed capture (hardware counter, no peak assumed)
                          "algorithmic": "n^3/3 + n^2 r + n r^2 FP64 flops per point (SURVEY §8(d)), "
                                         "x points per launch / launch duration (CUDA events on the launching stream), rank 0",
                          "share_of_step": chol_ms / (args.steps * ms_local) if ms_local else None},

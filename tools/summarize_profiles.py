@@ -50,6 +50,8 @@ for kern in ("chol", "build"):
         json.dump({"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                    "points_per_launch": pts, "dram_bytes_per_point": (rd + wr) / pts,
                    "duration_ms_under_ncu": float(m["gpu__time_duration.sum"][1]),
+                   "dmma_pipe_pct": g("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active"),
+                   "dmma_pipe_metric": "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active (same capture)",
                    "source": f"ncu --set full capture of chol_fused_kernel, profiles/{rnd}/ncu_chol_summary.txt"},
                   open(os.path.join(ROOT, "profiles", "chol_traffic.json"), "w"), indent=1)
 print(open(os.path.join(dst, "launch_shares.txt")).read())
