@@ -346,13 +346,17 @@ __global__ void __launch_bounds__(TABLE_NT) table_kernel(PointConst* __restrict_
         const double gs = quad_G(kap, sn * i4k, xs), gs2 = kLog2e * gs;
         double sum = 0.0;
         for (int c0 = 0; c0 < nq; c0 += QCAP) {
-          __syncwarp();
-          for (int j = lane; j < QCAP && c0 + j < nq; j += 32) {  // (a second pass recomputes
-            const double x = xl + (c0 + j) * h;                   //  the grid chunk by chunk)
-            double ex, em;
-            quad_exp(x, ex, em);
-            qa[j] = kLog2e * (kap * (x - em));  // base 2: the terms are 2^(G·log2 e)
-            qb[j] = kLog2e * (i4k / ex);
+          // the grid chunk (a grid that fits the scratch is generated once per unit, in the
+          // first pass; a longer one chunk by chunk in every pass)
+          if (pass == 0 || nq > QCAP) {
+            __syncwarp();
+            for (int j = lane; j < QCAP && c0 + j < nq; j += 32) {
+              const double x = xl + (c0 + j) * h;
+              double ex, em;
+              quad_exp(x, ex, em);
+              qa[j] = kLog2e * (kap * (x - em));  // base 2: the terms are 2^(G·log2 e)
+              qb[j] = kLog2e * (i4k / ex);
+            }
           }
           __syncwarp();
           const int cn = min(QCAP, nq - c0);
