@@ -38,7 +38,7 @@ def ctx():
     c.close()
 
 
-# C1 / C2 take the whole-octave table (n < 256), n300 the half-octave one (as C3-C5)
+# C1 / C2 take the whole-octave table (n < 256), n300 the quarter-octave one (as C3-C5)
 @pytest.mark.parametrize("name", ["C1", "C2", "n300"])
 def test_matern_build_extremes(ctx, orc, name):
     if name == "n300":

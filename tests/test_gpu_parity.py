@@ -109,7 +109,7 @@ def _inputs_n(n, K, seed=11):
     return coords, y, X, synthgen.make_params(cfg, K, seed=seed + 1), synthgen.make_lambdas(cfg.M)
 
 
-# C1 / C2 take the whole-octave table (n < 256), n300 the half-octave one (as C3-C5)
+# C1 / C2 take the whole-octave table (n < 256), n300 the quarter-octave one (as C3-C5)
 @pytest.mark.parametrize("name", ["C1", "C2", "n300"])
 def test_matern_build_elementwise(ctx, orc, name):
     coords, y, X, P, lam = _inputs_n(300, 64) if name == "n300" else synthgen.make_inputs(name, K=64)

@@ -87,7 +87,7 @@ def _mp_log_rho(kappa, z):
     return (1 - k) * mpmath.log(2) - mpmath.loggamma(k) + k * mpmath.log(z) + mpmath.log(mpmath.besselk(k, z))
 
 
-@pytest.mark.parametrize("n", [61, 300])  # both table layouts (whole octaves below n = 256, halves above)
+@pytest.mark.parametrize("n", [61, 300])  # both table layouts (whole octaves below n = 256, quarters above)
 def test_matern_build_vs_mpmath(ctx, n):
     """V[i, 0] = ρ(z_i) for sites on a line at x_i (φX = √(8κ), isotropic, so
     z_i = √(8κ)·x_i/φX ≈ x_i), z ∈ [1e-8, 700] log-spaced — through the table and the
