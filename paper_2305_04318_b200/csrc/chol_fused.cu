@@ -245,7 +245,37 @@ __device__ __forceinline__ void mma_chunk_any(Acc& acc, const double* Ab, int rb
 // each overwrites its own C group once computed.  The A fragment C[r][4s + lane%4]
 // is taken from the accumulator layout (C[r][8t + 2q + e] in lane (r, q), element e)
 // with two shuffles within the lane quad; k-steps above the triangle are skipped.
+#ifndef LIK_TRSM_PERM
+#define LIK_TRSM_PERM 1
+#endif
 __device__ __forceinline__ void trsm_reg(Acc& acc, const double* __restrict__ X, int lane) {
+#if LIK_TRSM_PERM
+  // The k (column-of-C) order of the product is free, so k-step (g, e) takes the columns
+  // 8g + 2t + e (t = lane mod 4): exactly the element e of column group g that the lane
+  // already holds in the accumulator layout — the A fragments come straight from the
+  // registers, no shuffles; B = L_jj⁻ᵀ is read in the same permuted order.
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int nt = NI - 1; nt >= 0; --nt) {
+    double o[MI][2];
+#pragma unroll
+    for (int m = 0; m < MI; ++m) o[m][0] = o[m][1] = 0.0;
+#pragma unroll
+    for (int g = 0; g <= nt; ++g) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double b = X[sw_off(8 * nt + lr, 8 * g + 2 * lc + e)];
+#pragma unroll
+        for (int m = 0; m < MI; ++m) dmma(o[m], acc[m][g][e], b);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MI; ++m) {
+      acc[m][nt][0] = o[m][0];
+      acc[m][nt][1] = o[m][1];
+    }
+  }
+#else
   const int lr = lane >> 2, lc = lane & 3, quad = lane & ~3, hi = lc >> 1;
   const bool odd = lc & 1;
 #pragma unroll
@@ -273,6 +303,7 @@ __device__ __forceinline__ void trsm_reg(Acc& acc, const double* __restrict__ X,
       acc[m][nt][1] = o[m][1];
     }
   }
+#endif
 }
 
 // acc = acc − T  (T = the A_ij tile in global memory), i.e. −C.
