@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(256, LIK_BUILD_MINB) build_kernel(const double
   if (P.mode == MODE_BAD) return;
   const int npad = g.nt * TB;
   __shared__ __align__(16) double2 sxy[2][TB];  // (x, y) of the tile's row and column sites
-  __shared__ __align__(16) double coef[TABLE_D];
+  extern __shared__ __align__(16) double coef[];  // the point's table (TABLE_D doubles, dynamic)
   __shared__ double etab[16];
   if (threadIdx.x < 16) etab[threadIdx.x] = kExp2Tab[threadIdx.x];
   // octaves [olo, oz] of the table; oz = the underflow octave (constant −2000) if built
@@ -627,11 +627,15 @@ cudaError_t launch_build(int sub, const double* coords, const SlotGeom& g, const
                          double* ws, cudaStream_t st) {
   const cudaTextureObject_t tex = table_tex;
   dim3 grid((g.ntri + g.nt + BUILD_TILES - 1) / BUILD_TILES, kw);
-  if (sub == CHEB_SUB_LARGE)
-    build_kernel<CHEB_SUB_LARGE><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
-  else
-    build_kernel<1><<<grid, 256, 0, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
-  return cudaGetLastError();
+  auto go = [&](auto kern, int table_d) -> cudaError_t {
+    const int smem = table_d * (int)sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 256, smem, st>>>(coords, g, pc, k0, table, Bt, ws, tex);
+    return cudaGetLastError();
+  };
+  if (sub == CHEB_SUB_LARGE) return go(build_kernel<CHEB_SUB_LARGE>, Cheb<CHEB_SUB_LARGE>::TABLE_D);
+  return go(build_kernel<1>, Cheb<1>::TABLE_D);
 }
 
 // ---------------------------------------------------------------------------
