@@ -174,3 +174,22 @@ def test_small_path_matches_fused_path(name, K):
     np.testing.assert_allclose(a["sigma2hat"][ok], b["sigma2hat"][ok], rtol=1e-10)
     sc = np.abs(b["betahat"][ok]).max(axis=-1, keepdims=True)
     assert (np.abs(a["betahat"][ok] - b["betahat"][ok]) / sc).max() <= 1e-9
+
+
+@pytest.mark.parametrize("name,K", [("C2", 400), ("swiss", 300)])
+def test_small_path_bitwise_repeatable_and_k_independent(ctx, name, K):
+    """chol_small (one CTA per point, matrix in shared memory): a point's outputs do not
+    depend on the other points of the call, its position in the grid, or the run —
+    bitwise, for the whole-octave table (one unit grid per three octaves) included."""
+    if name == "swiss":
+        cfg = synthgen.Config("sw", 100, 2, K, 34, True, "uniform", "swiss-shaped")
+        coords, y, X = synthgen.make_dataset(cfg, seed=5)
+        P, lam = synthgen.make_params(cfg, K, seed=6), np.linspace(-1.0, 2.0, 34)
+    else:
+        coords, y, X, P, lam = synthgen.make_inputs(name, K=K)
+    full = ctx.eval_batch(coords, y, X, P, lam)
+    again = ctx.eval_batch(coords, y, X, P, lam)
+    sub = ctx.eval_batch(coords, y, X, np.ascontiguousarray(P[K // 2:][::-1]), lam)
+    for key in full:
+        assert np.array_equal(full[key], again[key], equal_nan=True), key
+        assert np.array_equal(full[key][K // 2:][::-1], sub[key], equal_nan=True), key
