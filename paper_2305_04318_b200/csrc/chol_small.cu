@@ -51,6 +51,9 @@ __device__ __forceinline__ long long sph_clock() {
 #ifndef LIK_SMALL_PIV2
 #define LIK_SMALL_PIV2 1  // two pivots per step in the 8×8 factorisation (0: one; Swiss −0.7 %, C2 −0.5 %)
 #endif
+#ifndef LIK_SMALL_REGCHAIN
+#define LIK_SMALL_REGCHAIN 1  // dependent 8×8 products chained through the registers
+#endif
 #ifndef LIK_SMALL_UCH
 #define LIK_SMALL_UCH 2  // trailing-update tiles per chunk (C2 −6 %, Swiss −4 % against 4: the update competes less with the panel chain)
 #endif
@@ -338,6 +341,77 @@ __global__ void __launch_bounds__(NT, MINB)
     const int b = a + 1;  // b < T always (the B rows follow the V rows)
     // (a single-column panel, b ≥ Tv: column b is a Schur column and gets column a's
     // contribution from the step loop with the rest of the panel's update)
+#if LIK_SMALL_REGCHAIN
+    // Products whose left operand was just computed take it from the registers: with the
+    // k order of an 8×8 product permuted so that k-step e covers the columns 2t + e (t =
+    // lane mod 4), an operand in the accumulator layout (lane: row lane/4, columns 2t and
+    // 2t + 1) is its own A fragment — and, for X·Xᵀ, its own B fragment; a B operand in
+    // shared memory is read in the same order (bperm).  No store → load round trip
+    // between the dependent products of a row.
+    auto bperm = [&](const double* Y, int e) { return Y[toff(lane >> 2, 2 * (lane & 3) + e)]; };
+    if (g == NG - 1) {
+      factor8(tile(a, a), Wa, dlog + 8 * a, tol, &flag[0]);
+      __syncwarp();
+      double* Tba = tile(b, a);
+      double l[2] = {0.0, 0.0};  // L_ba = S_ba (−W_aa)ᵀ
+      {
+        const double x0 = frag_ab(Tba, lane, 0), x1 = frag_ab(Tba, lane, 1);
+        const double w0 = frag_ab(Wa, lane, 0), w1 = frag_ab(Wa, lane, 1);
+        dmma8(l, x0, w0);
+        dmma8(l, x1, w1);
+      }
+      __syncwarp();
+      *reinterpret_cast<double2*>(Tba + co) = make_double2(l[0], l[1]);
+      if (b < Tv) {
+        double* Tbb = tile(b, b);  // S_bb += L_ba L_baᵀ, both operands from the registers
+        const double2 cv = *reinterpret_cast<const double2*>(Tbb + co);
+        double c[2] = {cv.x, cv.y};
+        dmma8(c, l[0], l[0]);
+        dmma8(c, l[1], l[1]);
+        *reinterpret_cast<double2*>(Tbb + co) = make_double2(c[0], c[1]);
+        __syncwarp();
+        factor8(Tbb, Wb, dlog + 8 * b, tol, &flag[0]);
+      } else {
+        __syncwarp();
+      }
+    }
+    SPH(8);
+    g_bar();
+    SPH(9);
+    if (g < NG - 1) {
+      const double* Tba = tile(b, a);
+      double lb0 = 0.0, lb1 = 0.0, wb0 = 0.0, wb1 = 0.0;
+      if (b < Tv) {
+        lb0 = bperm(Tba, 0);
+        lb1 = bperm(Tba, 1);
+        wb0 = bperm(Wb, 0);
+        wb1 = bperm(Wb, 1);
+      }
+      const double wa0 = frag_ab(Wa, lane, 0), wa1 = frag_ab(Wa, lane, 1);
+      for (int i = a + 2 + g; i < T; i += NG - 1) {
+        double* Tia = tile(i, a);
+        double* Tib = tile(i, b);
+        const double x0 = frag_ab(Tia, lane, 0), x1 = frag_ab(Tia, lane, 1);
+        double2 cv = make_double2(0.0, 0.0);
+        if (b < Tv) cv = *reinterpret_cast<const double2*>(Tib + co);
+        double l[2] = {0.0, 0.0};  // L_ia = S_ia (−W_aa)ᵀ
+        dmma8(l, x0, wa0);
+        dmma8(l, x1, wa1);
+        __syncwarp();
+        *reinterpret_cast<double2*>(Tia + co) = make_double2(l[0], l[1]);
+        if (b < Tv) {
+          double c[2] = {cv.x, cv.y};  // S_ib += L_ia L_baᵀ
+          dmma8(c, l[0], lb0);
+          dmma8(c, l[1], lb1);
+          double o[2] = {0.0, 0.0};    // L_ib = S_ib (−W_bb)ᵀ
+          dmma8(o, c[0], wb0);
+          dmma8(o, c[1], wb1);
+          *reinterpret_cast<double2*>(Tib + co) = make_double2(o[0], o[1]);
+        }
+        __syncwarp();
+      }
+    }
+#else
     if (g == NG - 1) {
       factor8(tile(a, a), Wa, dlog + 8 * a, tol, &flag[0]);
       __syncwarp();
@@ -359,6 +433,7 @@ __global__ void __launch_bounds__(NT, MINB)
         }
       }
     }
+#endif
   };
   if (in_g) g_factor_solve(0);  // panel 0
   __syncthreads();
