@@ -155,10 +155,6 @@ __device__ __forceinline__ double exp2_neg(double y, const double* etab) {
   return m >= -1021 ? out : 0.0;
 }
 
-// High word of the first interval's centre 2^{LG+1} + 1 (3, 5, 9, 17 for SUB = 1, 2, 4, 8);
-// interval `part` adds 2·part, i.e. part << (20 − LG) in the high word.
-constexpr int centre_hi(int lg) { return ((1023 + lg + 1) << 20) | (1 << (20 - lg - 1)); }
-
 // Table evaluation of NE elements, interleaved (independent Horner chains for ILP).
 // s = z² from the point's scaled rotation (no square root); the octave o of s is
 // clamped to [olo, oz] (oz: the underflow octave, or ohi); elements whose octave lies
@@ -173,7 +169,6 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
                                                   const double (&hx)[NE], const double (&hy)[NE],
                                                   double (&v)[NE], unsigned& slow, int bit) {
   constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE, LG = Cheb<SUB>::LOG2SUB;
-  constexpr int kCentreHi = centre_hi(LG);
   double t[NE], h[NE];
   const double2* cp[NE];
 #pragma unroll
@@ -189,12 +184,12 @@ __device__ __forceinline__ void matern_rho_tableN(const PointConst& P, const dou
     // interval = SUB·octave + the top log2(SUB) mantissa bits: one shift of the high word;
     // clamped to [SUB·olo, SUB·oz + SUB − 1] (above: the underflow octave's constant)
     const int iv = min(max((hi >> (20 - LG)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
-    // t ∈ [−1, 1) from the mantissa alone: 2^{LG+1}·(1.mantissa) (exponent field set to
-    // 1023 + LG + 1) minus the interval's centre 2^{LG+1} + 1 + 2·part — exact
-    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + LG + 1) << 20), __double2loint(sv));
-    const int part = (hi >> (20 - LG)) & (SUB - 1);
-    const double centre = __hiloint2double(kCentreHi + (part << (20 - LG)), 0);
-    t[e] = m4 - centre;
+    // t ∈ [−1, 1) from the mantissa alone: the mantissa without its top LG bits (the
+    // interval) under the exponent field 1023 + LG + 1 is 2^{LG+1} + (the position in the
+    // interval) ∈ [2^{LG+1}, 2^{LG+1} + 2); minus the centre 2^{LG+1} + 1 — exact, one LOP3
+    // and one DADD
+    t[e] = __hiloint2double((hi & (0x000fffff >> LG)) | ((1023 + LG + 1) << 20), __double2loint(sv)) -
+           (double)((1 << (LG + 1)) + 1);
     cp[e] = reinterpret_cast<const double2*>(coef + iv * CHEB_STRIDE);
   }
 #ifdef LIK_BUILD_PREFETCH
@@ -252,7 +247,6 @@ __device__ __forceinline__ void matern_rho_tableN_tex(const PointConst& P, cudaT
                                                       const double (&hy)[NE], double (&v)[NE],
                                                       unsigned& slow, int bit) {
   constexpr int CHEB_N = Cheb<SUB>::N, CHEB_STRIDE = Cheb<SUB>::STRIDE, LG = Cheb<SUB>::LOG2SUB;
-  constexpr int kCentreHi = centre_hi(LG);
   double t[NE], h[NE];
   long long cp[NE];
   int ci[NE];
@@ -267,10 +261,8 @@ __device__ __forceinline__ void matern_rho_tableN_tex(const PointConst& P, cudaT
       slow |= (unsigned)((unsigned)(o - olo) > span) << (bit + e);
     }
     const int iv = min(max((hi >> (20 - LG)) - SUB * (1023 + CHEB_ELO), SUB * olo), SUB * oz + SUB - 1);
-    const double m4 = __hiloint2double((hi & 0x000fffff) | ((1023 + LG + 1) << 20), __double2loint(sv));
-    const int part = (hi >> (20 - LG)) & (SUB - 1);
-    const double centre = __hiloint2double(kCentreHi + (part << (20 - LG)), 0);
-    t[e] = m4 - centre;
+    t[e] = __hiloint2double((hi & (0x000fffff >> LG)) | ((1023 + LG + 1) << 20), __double2loint(sv)) -
+           (double)((1 << (LG + 1)) + 1);
     cp[e] = tbase + (long long)iv * (CHEB_STRIDE / 2);
     ci[e] = iv * CHEB_STRIDE;
   }
