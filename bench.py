@@ -125,6 +125,23 @@ def slot_bytes(n: int, r: int) -> int:
     return (nt * (nt + 1) // 2 + nt) * 64 * 64 * 8
 
 
+BUILD_INSTR_PER_ELEMENT = 81.6 / 32  # warp instructions per element, build_kernel<4> (ncu, profiles/r02/ncu_build_summary.txt)
+
+
+def build_issue_roofline(K, n, build_ms_per_step, sm_mhz, nsm=148):
+    """Issue-bound roofline of the Matérn build: elements (whole 64-tiles of the lower
+    tile triangle) x warp instructions per element over 4 sub-partitions x SMs x clock."""
+    if not build_ms_per_step or not sm_mhz:
+        return None
+    nt = (n + 63) // 64
+    elements = K * nt * (nt + 1) // 2 * 64 * 64
+    rate = elements * BUILD_INSTR_PER_ELEMENT / (build_ms_per_step / 1e3)  # warp instr/s
+    peak = 4 * nsm * sm_mhz * 1e6
+    return {"bound": "issue", "achieved": rate / 1e12, "peak": peak / 1e12, "unit": "Twarp-instr/s",
+            "frac": rate / peak, "instr_per_element": BUILD_INSTR_PER_ELEMENT,
+            "note": "table kernel time included (0.4 % of the stage)"}
+
+
 def hbm_peak():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
@@ -397,6 +414,7 @@ def main():
     if rank == 0:
         chol_ms, chol_n = stages["chol_fused"]
         build_ms, build_n = stages["matern_build"]
+        clk_med = clk.summary().get("sm_mhz")
         peak, peak_src = fp64_peak()
         achieved = (args.steps * K * F) / (chol_ms / 1e3) / 1e12 if chol_ms > 0 else None
         traffic, traffic_note, ncu_dmma = None, None, None
@@ -436,7 +454,11 @@ def main():
             "matern_build": {  # table + build per step: ρ evaluations and workspace bytes written
                 "evals_per_s": K * n * (n - 1) / 2 / (build_ms / args.steps / 1e3) if build_ms > 0 else None,
                 "gb_per_s_written": K * slot_bytes(n, r) / (build_ms / args.steps / 1e3) / 1e9 if build_ms > 0 else None,
-                "hbm_peak_gbs": hbm_peak()},
+                "hbm_peak_gbs": hbm_peak(),
+                # its bound is instruction issue: the build kernel's warp
+                # instructions per element from the committed ncu capture, against one
+                # issue per cycle on every SM sub-partition at the median SM clock
+                "issue_roofline": build_issue_roofline(K, n, build_ms / args.steps, clk_med)},
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
             "launches_per_step": {k: v[1] / args.steps for k, v in stages.items()},
             "gpu_launches": int(sum(v[1] for v in stages.values())),
