@@ -125,7 +125,7 @@ def slot_bytes(n: int, r: int) -> int:
     return (nt * (nt + 1) // 2 + nt) * 64 * 64 * 8
 
 
-BUILD_INSTR_PER_ELEMENT = 81.6 / 32  # warp instructions per element, build_kernel<4> (ncu, profiles/r02/ncu_build_summary.txt)
+BUILD_INSTR_PER_ELEMENT = 79.7 / 32  # warp instructions per element, build_kernel<4> (ncu, profiles/r02/ncu_build_summary.txt: 3.19e9 for 592 points)
 
 
 def build_issue_roofline(K, n, build_ms_per_step, sm_mhz, nsm=148):
