@@ -194,8 +194,10 @@ void lik_dataset_destroy(lik_dataset* ds);
  * multiple of 2 × #SMs except the last;
  * an explicit value is capped at 85 % of free HBM and at 65,535; if the
  * allocation fails, the wave is re-sized from a fresh free-memory query).  The workspace holds one
- * slot per wave point (C4: 17.9 MB).  Results do not depend on it
- * (determinism tests). */
+ * slot per wave point (C4: 17.9 MB).  Small matrices (8⌈n/8⌉ + 8⌈(M+p)/8⌉ ≤ 216 rows, the
+ * whole-octave table layout: n < 256) take the shared-memory path instead — one CTA per
+ * point builds and factors its matrix on chip, no workspace, waves of up to 65,535
+ * points.  Results do not depend on the wave size (determinism tests). */
 int lik_set_wave_points(lik_ctx* ctx, int points_per_wave);
 
 /* Debug / parity entry: the dense V = R + ν²I (n×n full, row-major) for each
